@@ -1,0 +1,191 @@
+/*
+ * bitdecode_b200.h -- C-ABI drop-in boundary for the BitDecoding decode hot
+ * path on B200 (sm_100a).  Plain C: pointers, sizes, status codes; no C++
+ * types, no torch types, no exceptions cross this boundary.
+ *
+ * Every entry point replaces one piece of the reference engine's C++ API
+ * (/root/reference/proj/include/bitkv, "bitkv::"), cited per function.  The
+ * C++ drop-in (include/bitkv_b200.hpp) and the Python binding
+ * (paper_2503_18773_b200/bitkv.py) re-expose the reference API on top of it;
+ * INTEGRATION.md shows how a reference-side caller binds it.
+ *
+ * Memory model: the cache lives in device memory (HBM) and is owned by the
+ * library.  Tensor arguments named *_dev are device pointers to binary16
+ * values (row-major, the reference shapes); *_host arguments are host fp32
+ * arrays holding binary16-representable values (the reference Tensor
+ * contract, tensor.hpp:16-46).  `stream` is a cudaStream_t (NULL = legacy
+ * default stream); device-pointer calls are stream-ordered and asynchronous.
+ */
+#ifndef BITDECODE_B200_H
+#define BITDECODE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define BDK_API __attribute__((visibility("default")))
+#else
+#define BDK_API
+#endif
+
+/* 1:1 with the reference exception classes (errors.hpp:14-54). */
+typedef enum bdk_status {
+  BDK_OK = 0,
+  BDK_CONFIG_ERROR = 1,     /* bitkv::ConfigError */
+  BDK_SHAPE_ERROR = 2,      /* bitkv::ShapeError */
+  BDK_UNSUPPORTED_BITS = 3, /* bitkv::UnsupportedBits */
+  BDK_CODE_OVERFLOW = 4,    /* bitkv::CodeOverflow */
+  BDK_CAPACITY_ERROR = 5,   /* bitkv::CapacityError */
+  BDK_STATE_ERROR = 6,      /* bitkv::StateError */
+  BDK_FORMAT_ERROR = 7,     /* bitkv::FormatError */
+  BDK_EMPTY_INPUT = 8,      /* bitkv::EmptyInput */
+  BDK_CUDA_ERROR = 20,      /* device / driver failure (message in bdk_last_error) */
+  BDK_UNSUPPORTED = 21,     /* geometry outside the sm_100a kernels' envelope */
+  BDK_INVALID_ARGUMENT = 22 /* NULL handle / pointer */
+} bdk_status;
+
+typedef struct bdk_cache bdk_cache;
+
+/* KVCache(batch, heads_kv, head_dim, warp_n, QuantSpec{num_bits, k_axis,
+ * group_size}, Contiguous, page_size, max_pages, interleave)
+ * (kvcache.hpp:107-109, quant.hpp:19-25).  max_tokens is the per-cell token
+ * capacity the device arena is sized for (the reference grows vectors). */
+typedef struct bdk_cache_desc {
+  uint32_t batch;
+  uint32_t heads_kv;
+  uint32_t head_dim;
+  uint32_t warp_n;
+  uint32_t num_bits;   /* 2, 4, 8, or 16 (fp16 passthrough) */
+  uint32_t k_axis;     /* 0 = QuantAxis::KChannel, 1 = QuantAxis::KToken */
+  uint32_t group_size;
+  uint32_t interleave; /* 1 = interleave_order, 0 = identity_order */
+  uint32_t max_tokens;
+  int32_t device;
+} bdk_cache_desc;
+
+/* AttentionConfig (config.hpp:13-25). */
+typedef struct bdk_attn_config {
+  uint32_t batch;
+  uint32_t heads_q;
+  uint32_t heads_kv;
+  uint32_t head_dim;
+  uint32_t tile_m;
+  uint32_t tile_n;
+  uint32_t num_splits;
+  uint32_t warp_n;
+  uint32_t warp_m;
+} bdk_attn_config;
+
+typedef struct bdk_cache_info {
+  uint32_t n_r;             /* KVCache::n_r(), residual_block_size (layout.cpp:74-77) */
+  uint32_t pack_num;        /* 16 / num_bits */
+  uint32_t words_per_block; /* u16 words per block per tensor */
+  uint32_t k_param_u16;     /* QuantParams::data.size() per block, K */
+  uint32_t v_param_u16;     /* ... V */
+  uint32_t record_bytes;    /* device block-record stride */
+  uint32_t max_blocks;      /* block slots per cell */
+  uint32_t fast_path;       /* 1 if the tensor-core decode kernel serves this geometry */
+} bdk_cache_info;
+
+/* ---------------------------------------------------------------- errors */
+BDK_API const char* bdk_last_error(void);         /* thread-local message */
+BDK_API const char* bdk_status_name(bdk_status s); /* "ConfigError", ... */
+
+/* validate_config (config.hpp:29, config.cpp:10-30) */
+BDK_API bdk_status bdk_validate_config(const bdk_attn_config* cfg);
+
+/* ------------------------------------------------------- cache lifetime */
+/* KVCache::KVCache (kvcache.cpp:114-148) */
+BDK_API bdk_status bdk_cache_create(const bdk_cache_desc* desc, bdk_cache** out);
+BDK_API bdk_status bdk_cache_destroy(bdk_cache* cache);
+BDK_API bdk_status bdk_cache_get_info(const bdk_cache* cache, bdk_cache_info* info);
+/* KVCache::packed_len / res_len (kvcache.hpp:145-147) */
+BDK_API bdk_status bdk_cache_lengths(const bdk_cache* cache, uint32_t b, uint32_t h,
+                                     uint32_t* packed_len, uint32_t* res_len);
+
+/* ------------------------------------------------- cache state machine */
+/* KVCache::prefill (kvcache.cpp:155-168): fused quantize+pack of the first
+ * len - len % N_r tokens (bit-exact), tail into the residual.
+ * k_dev/v_dev: binary16 [len][head_dim]. */
+BDK_API bdk_status bdk_prefill(bdk_cache* cache, uint32_t b, uint32_t h, const void* k_dev,
+                               const void* v_dev, uint32_t len, void* stream);
+/* prefill of every cell with the same length; k_dev/v_dev:
+ * [batch][heads_kv][len][head_dim] (run_bench's prefill loop,
+ * bench.cpp:132-139, in one launch). */
+BDK_API bdk_status bdk_prefill_all(bdk_cache* cache, const void* k_dev, const void* v_dev,
+                                   uint32_t len, void* stream);
+/* KVCache::append_token (kvcache.cpp:170-182); rows binary16 [head_dim]. */
+BDK_API bdk_status bdk_append_token(bdk_cache* cache, uint32_t b, uint32_t h,
+                                    const void* k_row_dev, const void* v_row_dev, void* stream);
+/* KVCache::flush_residual (kvcache.cpp:245-251). */
+BDK_API bdk_status bdk_flush_residual(bdk_cache* cache, uint32_t b, uint32_t h, void* stream);
+
+/* ----------------------------------------------------------- decode step */
+/* decode_step (attention.hpp:87-88, attention.cpp:164-242): append the new
+ * token of every cell, residual + packed split-KV attention, LSE combine,
+ * commit of any full residual block.
+ * q_dev [batch][heads_q][d], k_new_dev/v_new_dev [batch][heads_kv][d]
+ * (binary16), out_dev fp32 [batch][heads_q][d]. */
+BDK_API bdk_status bdk_decode_step(bdk_cache* cache, const bdk_attn_config* cfg,
+                                   const void* q_dev, const void* k_new_dev,
+                                   const void* v_new_dev, float* out_dev, void* stream);
+/* Same contract with host fp32 tensors (the reference's by-value Tensor /
+ * AttnOutput interface); synchronous; host<->device copies included. */
+BDK_API bdk_status bdk_decode_step_host(bdk_cache* cache, const bdk_attn_config* cfg,
+                                        const float* q_host, const float* k_new_host,
+                                        const float* v_new_host, float* out_host);
+/* Partial decode for sequence-split multi-GPU: attends packed blocks
+ * [blk_begin, blk_end) of every cell plus the residual; appends only when
+ * k_new_dev != NULL.  Writes the NORMALIZED partial output out_dev
+ * [batch][heads_q][d] and its log2-sum-exp lse_dev [batch][heads_q]; the
+ * partials of all ranks merge with bdk_merge_partials (combine,
+ * attention.cpp:142-162). */
+BDK_API bdk_status bdk_decode_partial(bdk_cache* cache, const bdk_attn_config* cfg,
+                                      const void* q_dev, const void* k_new_dev,
+                                      const void* v_new_dev, uint32_t blk_begin,
+                                      uint32_t blk_end, float* out_dev, float* lse_dev,
+                                      void* stream);
+/* o_dev [n_parts][rows][d], lse_dev [n_parts][rows] -> out_dev [rows][d] */
+BDK_API bdk_status bdk_merge_partials(const float* o_dev, const float* lse_dev, uint32_t n_parts,
+                                      uint32_t rows, uint32_t d, float* out_dev, void* stream);
+/* 0 = fast (fp16 P), 1 = precise PV (P = P_hi + P_lo) */
+BDK_API bdk_status bdk_set_precise(bdk_cache* cache, int precise);
+
+/* --------------------------------------------------------- readback/IO */
+/* PackedBlock of cell (b, h) (kvcache.hpp:17-26) in the reference layout
+ * (kvcache.cpp:79-95, quant.cpp:71/:88), host outputs; any pointer may be
+ * NULL.  Sizes from bdk_cache_get_info. */
+BDK_API bdk_status bdk_read_block(const bdk_cache* cache, uint32_t b, uint32_t h, uint32_t blk,
+                                  uint16_t* k_words, uint16_t* v_words, uint16_t* k_params,
+                                  uint16_t* v_params);
+/* KVCache::adopt_block (kvcache.cpp:239-243): append an already-packed block
+ * (reference layout, host inputs). */
+BDK_API bdk_status bdk_adopt_block(bdk_cache* cache, uint32_t b, uint32_t h,
+                                   const uint16_t* k_words, const uint16_t* v_words,
+                                   const uint16_t* k_params, const uint16_t* v_params);
+/* KVCache::residual_tile (kvcache.cpp:253-261) as binary16 bits, host
+ * [res_len][d] each. */
+BDK_API bdk_status bdk_read_residual(const bdk_cache* cache, uint32_t b, uint32_t h,
+                                     uint16_t* k_host, uint16_t* v_host);
+/* KVCache::packed_tile dequant (kvcache.cpp:263-312) of blocks [blk0,
+ * blk0+nblk) into binary16 device rows [nblk*N_r][d]. */
+BDK_API bdk_status bdk_dequant_blocks(const bdk_cache* cache, uint32_t b, uint32_t h,
+                                      uint32_t blk0, uint32_t nblk, void* k_out_dev,
+                                      void* v_out_dev, void* stream);
+/* KVCache::memory (kvcache.cpp:330-345): {k payload, v payload, params,
+ * residual} bytes. */
+BDK_API bdk_status bdk_memory(const bdk_cache* cache, uint64_t out[4]);
+/* KVCache::corrupt_word (kvcache.cpp:326-328): fault injection on K words. */
+BDK_API bdk_status bdk_corrupt_word(bdk_cache* cache, uint32_t b, uint32_t h, uint32_t blk,
+                                    uint32_t word, uint16_t value);
+/* Blocks until all work on the cache's device is done; reports async errors. */
+BDK_API bdk_status bdk_synchronize(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BITDECODE_B200_H */

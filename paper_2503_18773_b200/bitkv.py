@@ -1,0 +1,466 @@
+"""Host-side mirror of the reference ``bitkv::`` API over the sm_100a C-ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/bitkv (cited per symbol) so tests read like the
+reference's doctest suites.  The cache lives in HBM; every numeric step
+(quantize+pack, dequant, attention, combine) runs in the CUDA kernels behind
+include/bitdecode_b200.h.  Host-side code only converts layouts, checks the
+reference preconditions and moves bytes.
+
+Tensor arguments accept either CUDA ``torch.float16`` tensors (used in place,
+stream-ordered on the current torch stream) or host arrays of
+binary16-representable fp32 values (the reference Tensor contract,
+tensor.hpp:16-46), which are uploaded.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as _L
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is the device-memory plumbing
+    torch = None
+
+
+# --------------------------------------------------------------- errors.hpp
+class Error(RuntimeError):
+    """bitkv::Error (errors.hpp:9-12)."""
+
+
+class ConfigError(Error):
+    pass
+
+
+class ShapeError(Error):
+    pass
+
+
+class UnsupportedBits(Error):
+    pass
+
+
+class CodeOverflow(Error):
+    pass
+
+
+class CapacityError(Error):
+    pass
+
+
+class StateError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class EmptyInput(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+class Unsupported(Error):
+    pass
+
+
+_STATUS = {1: ConfigError, 2: ShapeError, 3: UnsupportedBits, 4: CodeOverflow, 5: CapacityError,
+           6: StateError, 7: FormatError, 8: EmptyInput, 20: CudaError, 21: Unsupported,
+           22: Error}
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = _L.load().bdk_last_error().decode(errors="replace")
+        raise _STATUS.get(status, Error)(msg)
+
+
+# ----------------------------------------------------------------- quant.hpp
+class QuantAxis(enum.IntEnum):
+    """quant.hpp:12-15"""
+    KChannel = 0
+    KToken = 1
+
+
+@dataclass
+class QuantSpec:
+    """quant.hpp:19-25"""
+    num_bits: int = 4
+    k_axis: QuantAxis = QuantAxis.KChannel
+    group_size: int = 64
+
+    def passthrough(self) -> bool:
+        return self.num_bits == 16
+
+
+class CacheBackend(enum.IntEnum):
+    """kvcache.hpp:100 (the paged backend is host bookkeeping)."""
+    Contiguous = 0
+    Paged = 1
+
+
+# ---------------------------------------------------------------- config.hpp
+@dataclass
+class AttentionConfig:
+    """config.hpp:13-25"""
+    batch: int = 1
+    heads_q: int = 32
+    heads_kv: int = 8
+    head_dim: int = 128
+    tile_m: int = 1
+    tile_n: int = 64
+    num_splits: int = 1
+    warp_n: int = 4
+    warp_m: int = 1
+
+    def n_group(self) -> int:
+        return self.heads_q // self.heads_kv
+
+    def _c(self) -> _L.AttnConfig:
+        return _L.AttnConfig(self.batch, self.heads_q, self.heads_kv, self.head_dim, self.tile_m,
+                             self.tile_n, self.num_splits, self.warp_n, self.warp_m)
+
+
+def validate_config(cfg: AttentionConfig) -> AttentionConfig:
+    """validate_config (config.hpp:29, config.cpp:10-30)."""
+    c = cfg._c()
+    _check(_L.load().bdk_validate_config(C.byref(c)))
+    return cfg
+
+
+def residual_block_size(num_bits: int, warp_n: int) -> int:
+    """layout.cpp:74-77: N_r = 8 * W_n * (16 / B)."""
+    if num_bits not in (2, 4, 8, 16):
+        raise UnsupportedBits(f"num_bits must be one of 2, 4, 8, 16; got {num_bits}")
+    return 8 * warp_n * (16 // num_bits)
+
+
+# --------------------------------------------------------------- kvcache.hpp
+@dataclass
+class PackedBlock:
+    """kvcache.hpp:17-26 (u16 arrays in the reference layout)."""
+    k_words: np.ndarray
+    v_words: np.ndarray
+    k_params: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint16))
+    v_params: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint16))
+
+    def __eq__(self, other) -> bool:
+        return all(np.array_equal(getattr(self, f), getattr(other, f))
+                   for f in ("k_words", "v_words", "k_params", "v_params"))
+
+
+@dataclass
+class Memory:
+    """KVCache::Memory (kvcache.hpp:165-171)."""
+    k_packed_payload_bytes: int
+    v_packed_payload_bytes: int
+    params_bytes: int
+    residual_bytes: int
+
+
+def _u16p(a: np.ndarray):
+    return a.ctypes.data_as(_L.u16p) if a is not None and a.size else None
+
+
+def _stream_ptr():
+    if torch is not None and torch.cuda.is_available():
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return None
+
+
+def _as_f16_cuda(x, shape=None, device=0):
+    """torch CUDA fp16 contiguous view of x (kept alive by the caller)."""
+    if torch is None:
+        raise Error("torch is required for device memory plumbing")
+    if isinstance(x, torch.Tensor):
+        t = x
+        if not t.is_cuda:
+            t = t.to(f"cuda:{device}")
+        if t.dtype != torch.float16:
+            t = t.to(torch.float16)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(f"cuda:{device}").half()
+    t = t.contiguous()
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        if t.numel() != math.prod(shape):
+            raise ShapeError(f"expected shape {tuple(shape)}, got {tuple(t.shape)}")
+        t = t.reshape(shape)
+    return t
+
+
+class KVCache:
+    """bitkv::KVCache (kvcache.hpp:103-189) with the packed segment and the
+    residual window resident in HBM.  ``max_tokens`` sizes the per-cell arena
+    (the reference grows host vectors instead)."""
+
+    def __init__(self, batch: int, heads_kv: int, head_dim: int, warp_n: int,
+                 spec: QuantSpec | None = None, backend: CacheBackend = CacheBackend.Contiguous,
+                 page_size: int = 16, max_pages: int = 0, interleave: bool = True, *,
+                 max_tokens: int = 1 << 16, device: int = 0):
+        spec = spec or QuantSpec()
+        self._h = None
+        if backend == CacheBackend.Paged:
+            n_r = residual_block_size(spec.num_bits, warp_n)
+            if page_size == 0 or n_r % page_size:
+                raise ConfigError(f"page_size ({page_size}) must divide N_r ({n_r})")
+        desc = _L.CacheDesc(batch, heads_kv, head_dim, warp_n, spec.num_bits, int(spec.k_axis),
+                            spec.group_size, 1 if interleave else 0, max_tokens, device)
+        h = C.c_void_p()
+        _check(_L.load().bdk_cache_create(C.byref(desc), C.byref(h)))
+        self._h = h
+        self._batch, self._heads_kv, self._d, self._warp_n = batch, heads_kv, head_dim, warp_n
+        self._spec, self._interleave, self._device = spec, bool(interleave), device
+        self._backend, self._page_size = backend, page_size
+        info = _L.CacheInfo()
+        _check(_L.load().bdk_cache_get_info(self._h, C.byref(info)))
+        self.info = info
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            try:
+                _L.load().bdk_cache_destroy(self._h)
+            except Exception:
+                pass
+            self._h = None
+
+    # accessors (kvcache.hpp:111-121)
+    def batch(self) -> int:
+        return self._batch
+
+    def heads_kv(self) -> int:
+        return self._heads_kv
+
+    def head_dim(self) -> int:
+        return self._d
+
+    def warp_n(self) -> int:
+        return self._warp_n
+
+    def n_r(self) -> int:
+        return self.info.n_r
+
+    def spec(self) -> QuantSpec:
+        return self._spec
+
+    def backend(self) -> CacheBackend:
+        return self._backend
+
+    def interleaved(self) -> bool:
+        return self._interleave
+
+    def handle(self):
+        return self._h
+
+    # state machine (kvcache.hpp:123-143)
+    def prefill(self, b: int, h: int, k, v, length: int | None = None) -> None:
+        """KVCache::prefill (kvcache.cpp:155-168); k, v: [len, d]."""
+        k = _as_f16_cuda(k, device=self._device).reshape(-1, self._d)
+        v = _as_f16_cuda(v, device=self._device).reshape(-1, self._d)
+        n = k.shape[0] if length is None else length
+        _check(_L.load().bdk_prefill(self._h, b, h, C.c_void_p(k.data_ptr()),
+                                     C.c_void_p(v.data_ptr()), n, _stream_ptr()))
+        self._keep = (k, v)
+
+    def prefill_all(self, k, v) -> None:
+        """All cells at once; k, v: [batch, heads_kv, len, d] (CUDA fp16)."""
+        k = _as_f16_cuda(k, device=self._device)
+        v = _as_f16_cuda(v, device=self._device)
+        _check(_L.load().bdk_prefill_all(self._h, C.c_void_p(k.data_ptr()),
+                                         C.c_void_p(v.data_ptr()), k.shape[-2], _stream_ptr()))
+        self._keep = (k, v)
+
+    def append_token(self, b: int, h: int, k_row, v_row) -> None:
+        """KVCache::append_token (kvcache.cpp:170-182)."""
+        k = _as_f16_cuda(k_row, (self._d,), self._device)
+        v = _as_f16_cuda(v_row, (self._d,), self._device)
+        _check(_L.load().bdk_append_token(self._h, b, h, C.c_void_p(k.data_ptr()),
+                                          C.c_void_p(v.data_ptr()), _stream_ptr()))
+        self._keep = (k, v)
+
+    def flush_residual(self, b: int, h: int) -> None:
+        """KVCache::flush_residual (kvcache.cpp:245-251)."""
+        _check(_L.load().bdk_flush_residual(self._h, b, h, _stream_ptr()))
+
+    def adopt_block(self, b: int, h: int, block: PackedBlock) -> None:
+        """KVCache::adopt_block (kvcache.cpp:239-243)."""
+        kw = np.ascontiguousarray(block.k_words, np.uint16)
+        vw = np.ascontiguousarray(block.v_words, np.uint16)
+        kp = np.ascontiguousarray(block.k_params, np.uint16)
+        vpp = np.ascontiguousarray(block.v_params, np.uint16)
+        _check(_L.load().bdk_adopt_block(self._h, b, h, _u16p(kw), _u16p(vw), _u16p(kp),
+                                         _u16p(vpp)))
+
+    def _lengths(self, b, h):
+        p, r = C.c_uint32(), C.c_uint32()
+        _check(_L.load().bdk_cache_lengths(self._h, b, h, C.byref(p), C.byref(r)))
+        return p.value, r.value
+
+    def packed_len(self, b: int, h: int) -> int:
+        return self._lengths(b, h)[0]
+
+    def res_len(self, b: int, h: int) -> int:
+        return self._lengths(b, h)[1]
+
+    def total_len(self, b: int, h: int) -> int:
+        p, r = self._lengths(b, h)
+        return p + r
+
+    # readback (kvcache.hpp:145-160)
+    def block(self, b: int, h: int, i: int) -> PackedBlock:
+        kw = np.zeros(self.info.words_per_block, np.uint16)
+        vw = np.zeros(self.info.words_per_block, np.uint16)
+        kp = np.zeros(self.info.k_param_u16, np.uint16)
+        vpp = np.zeros(self.info.v_param_u16, np.uint16)
+        _check(_L.load().bdk_read_block(self._h, b, h, i, _u16p(kw), _u16p(vw), _u16p(kp),
+                                        _u16p(vpp)))
+        return PackedBlock(kw, vw, kp, vpp)
+
+    def packed(self, b: int, h: int) -> list[PackedBlock]:
+        """KVCache::packed(b, h).blocks (kvcache.hpp:148)."""
+        return [self.block(b, h, i) for i in range(self.packed_len(b, h) // self.n_r())]
+
+    def residual_tile(self, b: int, h: int):
+        """KVCache::residual_tile (kvcache.cpp:253-261) -> fp32 [res_len, d] x2."""
+        r = self.res_len(b, h)
+        k = np.zeros(r * self._d, np.uint16)
+        v = np.zeros(r * self._d, np.uint16)
+        _check(_L.load().bdk_read_residual(self._h, b, h, _u16p(k), _u16p(v)))
+        return (k.view(np.float16).astype(np.float32).reshape(r, self._d),
+                v.view(np.float16).astype(np.float32).reshape(r, self._d))
+
+    def packed_tile(self, b: int, h: int, t0: int, length: int):
+        """KVCache::packed_tile (kvcache.cpp:263-312), dequantized on device."""
+        n_r = self.n_r()
+        if t0 + length > self.packed_len(b, h):
+            raise ShapeError("packed_tile: range past packed segment")
+        if length == 0:
+            z = np.zeros((0, self._d), np.float32)
+            return z, z.copy()
+        blk0, blk1 = t0 // n_r, (t0 + length + n_r - 1) // n_r
+        nb = blk1 - blk0
+        kd = torch.empty((nb * n_r, self._d), dtype=torch.float16, device=f"cuda:{self._device}")
+        vd = torch.empty_like(kd)
+        _check(_L.load().bdk_dequant_blocks(self._h, b, h, blk0, nb, C.c_void_p(kd.data_ptr()),
+                                            C.c_void_p(vd.data_ptr()), _stream_ptr()))
+        off = t0 - blk0 * n_r
+        return (kd[off:off + length].float().cpu().numpy(),
+                vd[off:off + length].float().cpu().numpy())
+
+    def reconstruct(self, b: int, h: int):
+        """KVCache::reconstruct (kvcache.cpp:314-324)."""
+        plen = self.packed_len(b, h)
+        pk, pv = self.packed_tile(b, h, 0, plen)
+        rk, rv = self.residual_tile(b, h)
+        return np.concatenate([pk, rk]), np.concatenate([pv, rv])
+
+    def corrupt_word(self, b: int, h: int, block: int, word: int, value: int) -> None:
+        """KVCache::corrupt_word (kvcache.cpp:326-328)."""
+        _check(_L.load().bdk_corrupt_word(self._h, b, h, block, word, value))
+
+    def memory(self) -> Memory:
+        """KVCache::memory (kvcache.cpp:330-345)."""
+        out = (C.c_uint64 * 4)()
+        _check(_L.load().bdk_memory(self._h, out))
+        return Memory(*[int(x) for x in out])
+
+    def set_precise(self, precise: bool) -> None:
+        """fp16 P (False) or P_hi + P_lo split PV (True), SURVEY.md F4."""
+        _check(_L.load().bdk_set_precise(self._h, 1 if precise else 0))
+
+
+# ------------------------------------------------------------ attention.hpp
+@dataclass
+class AttnOutput:
+    """attention.hpp:73-84: fp32 [batch, heads, d]."""
+    batch: int
+    heads: int
+    d: int
+    data: object  # torch CUDA tensor (device path) or numpy array (host path)
+
+    def row(self, b: int, h: int):
+        return self.data[b, h]
+
+
+def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None) -> AttnOutput:
+    """decode_step (attention.hpp:87-88, attention.cpp:164-242).
+
+    CUDA fp16 tensors in -> CUDA fp32 ``out`` (stream-ordered, no sync).
+    Host arrays in -> numpy out via the host C-ABI entry (H2D/D2H inside)."""
+    c = cfg._c()
+    shape_q = (cfg.batch, cfg.heads_q, cfg.head_dim)
+    shape_kv = (cfg.batch, cfg.heads_kv, cfg.head_dim)
+    is_dev = torch is not None and isinstance(q, torch.Tensor) and q.is_cuda
+    if not is_dev:
+        qh = np.ascontiguousarray(q, np.float32)
+        kh = np.ascontiguousarray(k_new, np.float32)
+        vh = np.ascontiguousarray(v_new, np.float32)
+        if qh.shape != shape_q or kh.shape != shape_kv or vh.shape != shape_kv:
+            validate_config(cfg)
+            raise ShapeError("decode_step: q must be [batch, heads_q, d], k_new/v_new "
+                             "[batch, heads_kv, d]")
+        o = np.zeros(shape_q, np.float32)
+        fpp = lambda a: a.ctypes.data_as(_L.fp)  # noqa: E731
+        _check(_L.load().bdk_decode_step_host(cache.handle(), C.byref(c), fpp(qh), fpp(kh),
+                                              fpp(vh), fpp(o)))
+        return AttnOutput(cfg.batch, cfg.heads_q, cfg.head_dim, o)
+    if tuple(q.shape) != shape_q or tuple(k_new.shape) != shape_kv or \
+            tuple(v_new.shape) != shape_kv:
+        validate_config(cfg)
+        raise ShapeError("decode_step: q must be [batch, heads_q, d], k_new/v_new "
+                         "[batch, heads_kv, d]")
+    qd, kd, vd = (_as_f16_cuda(x) for x in (q, k_new, v_new))
+    if out is None:
+        out = torch.empty(shape_q, dtype=torch.float32, device=q.device)
+    _check(_L.load().bdk_decode_step(cache.handle(), C.byref(c), C.c_void_p(qd.data_ptr()),
+                                     C.c_void_p(kd.data_ptr()), C.c_void_p(vd.data_ptr()),
+                                     C.c_void_p(out.data_ptr()), _stream_ptr()))
+    return AttnOutput(cfg.batch, cfg.heads_q, cfg.head_dim, out)
+
+
+def decode_partial(cache: KVCache, cfg: AttentionConfig, q, k_new=None, v_new=None,
+                   blk_begin: int = 0, blk_end: int = 1 << 30):
+    """Sequence-split partial (see bdk_decode_partial): returns the normalized
+    partial output [batch, heads_q, d] and its log2-sum-exp [batch, heads_q]."""
+    c = cfg._c()
+    qd = _as_f16_cuda(q)
+    kd = _as_f16_cuda(k_new) if k_new is not None else None
+    vd = _as_f16_cuda(v_new) if v_new is not None else None
+    o = torch.empty((cfg.batch, cfg.heads_q, cfg.head_dim), dtype=torch.float32,
+                    device=qd.device)
+    lse = torch.empty((cfg.batch, cfg.heads_q), dtype=torch.float32, device=qd.device)
+    _check(_L.load().bdk_decode_partial(
+        cache.handle(), C.byref(c), C.c_void_p(qd.data_ptr()),
+        C.c_void_p(kd.data_ptr()) if kd is not None else None,
+        C.c_void_p(vd.data_ptr()) if vd is not None else None, blk_begin,
+        min(blk_end, (1 << 32) - 1), C.c_void_p(o.data_ptr()), C.c_void_p(lse.data_ptr()),
+        _stream_ptr()))
+    return o, lse
+
+
+def merge_partials(o_parts, lse_parts):
+    """combine (attention.cpp:142-162) of normalized partials:
+    o_parts [n, rows..., d], lse_parts [n, rows...] (CUDA fp32)."""
+    n = o_parts.shape[0]
+    d = o_parts.shape[-1]
+    rows = lse_parts[0].numel()
+    o_parts = o_parts.contiguous().float()
+    lse_parts = lse_parts.contiguous().float()
+    out = torch.empty(o_parts.shape[1:], dtype=torch.float32, device=o_parts.device)
+    _check(_L.load().bdk_merge_partials(C.c_void_p(o_parts.data_ptr()),
+                                        C.c_void_p(lse_parts.data_ptr()), n, rows, d,
+                                        C.c_void_p(out.data_ptr()), _stream_ptr()))
+    return out
+
+
+def synchronize() -> None:
+    _check(_L.load().bdk_synchronize())

@@ -1,0 +1,619 @@
+// bdk_api.cu -- host implementation of the C-ABI (include/bitdecode_b200.h).
+//
+// Owns the device arena of one cache and an authoritative host mirror of the
+// per-cell lengths (packed blocks, residual fill).  The mirror drives the
+// reference's precondition checks (StateError / CapacityError / ShapeError,
+// kvcache.cpp:155-251, attention.cpp:164-179) before any launch, and the
+// split planning of the decode grid.  No exception crosses the boundary and
+// there is no host compute path: every numeric step runs in the sm_100a
+// kernels of bdk_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bitdecode_b200.h"
+#include "bdk_launch.h"
+
+using bdk::DevCache;
+using bdk::Geom;
+
+struct bdk_cache {
+  DevCache dev;
+  bdk_cache_desc desc{};
+  int device = 0;
+  int num_sms = 148;
+  int precise = 0;
+  uint32_t kp_u16 = 0, vp_u16 = 0, wpb = 0;
+  std::vector<int> packed_blocks, res_len;  // host mirror
+  // decode workspace
+  float* part_o = nullptr;
+  float* part_ml = nullptr;
+  size_t part_floats = 0, part_ml_floats = 0;
+  // host-API staging (pinned host + device)
+  void* h_stage = nullptr;
+  void* d_stage = nullptr;
+  size_t stage_bytes = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+bdk_status fail(bdk_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+bdk_status cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return BDK_CUDA_ERROR;
+}
+
+#define BDK_CUDA(call, where)                  \
+  do {                                         \
+    cudaError_t e_ = (call);                   \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int cell_of(const bdk_cache* c, uint32_t b, uint32_t h) {
+  return static_cast<int>(b * c->desc.heads_kv + h);
+}
+
+bdk_status check_cell(const bdk_cache* c, uint32_t b, uint32_t h) {
+  if (!c) return fail(BDK_INVALID_ARGUMENT, "null cache");
+  if (b >= c->desc.batch || h >= c->desc.heads_kv)
+    return fail(BDK_SHAPE_ERROR, "cell index out of range");
+  return BDK_OK;
+}
+
+uint32_t param_u16(uint32_t n_r, uint32_t d, uint32_t bits, uint32_t axis, uint32_t g) {
+  if (bits == 16) return 0;
+  const uint32_t groups = axis == 0 ? (n_r / g) * d : n_r * (d / g);
+  return 2 * groups;  // (scale, zero) halves, quant.hpp:38-47
+}
+
+size_t word_offset(const Geom& G, uint32_t word) {
+  // logical word index -> byte offset inside the swizzled word array
+  const uint32_t per_row = 8 * G.warp_n;
+  const uint32_t c = word / per_row, wi = word % per_row, j = wi / 8;
+  return (size_t)c * 16 * G.warp_n + ((j ^ bdk::swz(c, G.warp_n)) << 4) + (wi % 8) * 2;
+}
+
+bdk_status ensure_workspace(bdk_cache* c, int n_parts, int ng) {
+  const size_t cells = (size_t)c->desc.batch * c->desc.heads_kv;
+  const size_t need = cells * n_parts * ng * c->desc.head_dim;
+  const size_t need_ml = cells * n_parts * ng * 2;
+  if (need > c->part_floats) {
+    if (c->part_o) cudaFree(c->part_o);
+    c->part_o = nullptr;
+    BDK_CUDA(cudaMalloc(&c->part_o, need * sizeof(float)), "cudaMalloc(partials)");
+    c->part_floats = need;
+  }
+  if (need_ml > c->part_ml_floats) {
+    if (c->part_ml) cudaFree(c->part_ml);
+    c->part_ml = nullptr;
+    BDK_CUDA(cudaMalloc(&c->part_ml, need_ml * sizeof(float)), "cudaMalloc(partials)");
+    c->part_ml_floats = need_ml;
+  }
+  return BDK_OK;
+}
+
+bdk_status ensure_stage(bdk_cache* c, size_t bytes) {
+  if (bytes <= c->stage_bytes) return BDK_OK;
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  if (c->d_stage) cudaFree(c->d_stage);
+  c->h_stage = c->d_stage = nullptr;
+  BDK_CUDA(cudaMallocHost(&c->h_stage, bytes), "cudaMallocHost(stage)");
+  BDK_CUDA(cudaMalloc(&c->d_stage, bytes), "cudaMalloc(stage)");
+  c->stage_bytes = bytes;
+  return BDK_OK;
+}
+
+bdk_status validate(const bdk_attn_config* cfg) {
+  auto req = [](bool ok, const char* what) { return ok ? BDK_OK : fail(BDK_CONFIG_ERROR, what); };
+  bdk_status s;
+  if ((s = req(cfg->batch > 0, "batch must be > 0"))) return s;
+  if ((s = req(cfg->heads_q > 0, "heads_q must be > 0"))) return s;
+  if ((s = req(cfg->heads_kv > 0, "heads_kv must be > 0"))) return s;
+  if ((s = req(cfg->head_dim > 0, "head_dim must be > 0"))) return s;
+  if ((s = req(cfg->tile_m > 0, "tile_m must be > 0"))) return s;
+  if ((s = req(cfg->tile_n > 0, "tile_n must be > 0"))) return s;
+  if ((s = req(cfg->num_splits >= 1, "num_splits must be >= 1"))) return s;
+  if ((s = req(cfg->warp_n > 0, "warp_n must be > 0"))) return s;
+  if ((s = req(cfg->warp_m > 0, "warp_m must be > 0"))) return s;
+  if ((s = req(cfg->heads_q % cfg->heads_kv == 0, "heads_q must be divisible by heads_kv")))
+    return s;
+  if ((s = req(cfg->tile_n % (cfg->warp_n * 8) == 0, "tile_n must be divisible by warp_n*8")))
+    return s;
+  return BDK_OK;
+}
+
+// decode_step shape checks (attention.cpp:164-179) + capacity of the append
+bdk_status check_decode(bdk_cache* c, const bdk_attn_config* cfg, bool appends) {
+  if (!c || !cfg) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  bdk_status s = validate(cfg);
+  if (s) return s;
+  if (cfg->batch != c->desc.batch || cfg->heads_kv != c->desc.heads_kv ||
+      cfg->head_dim != c->desc.head_dim)
+    return fail(BDK_SHAPE_ERROR, "decode_step: cache geometry does not match config");
+  if (cfg->heads_q / cfg->heads_kv > 8)
+    return fail(BDK_UNSUPPORTED, "n_group > 8 is outside the decode kernel envelope");
+  if (appends) {
+    const int n_r = c->dev.G.n_r;
+    for (size_t i = 0; i < c->res_len.size(); ++i) {
+      if (c->res_len[i] == n_r)
+        return fail(BDK_CAPACITY_ERROR, "residual is full; flush before appending");
+      if (c->res_len[i] + 1 == n_r && c->packed_blocks[i] >= c->dev.G.max_blocks)
+        return fail(BDK_CAPACITY_ERROR, "cache arena full (raise max_tokens)");
+    }
+  }
+  return BDK_OK;
+}
+
+bdk_status run_decode(bdk_cache* c, const bdk_attn_config* cfg, const void* q, const void* k_new,
+                      const void* v_new, float* out, float* lse, int blk_begin, int blk_end,
+                      cudaStream_t stream) {
+  const int cells = static_cast<int>(c->desc.batch * c->desc.heads_kv);
+  int nblk_max = 0;
+  for (int i = 0; i < cells; ++i) nblk_max = std::max(nblk_max, c->packed_blocks[i]);
+  const int lo = std::max(0, blk_begin), hi = std::min(blk_end, nblk_max);
+  const int span = std::max(0, hi - lo);
+  // split planning: ~3 resident CTAs per SM worth of packed blocks, <= 256
+  // splits per cell (attention.cpp:116-130 splits on the CPU; the GPU picks
+  // its own -- results are split-invariant, test_attention.cpp:312-340)
+  const long target = (long)c->num_sms * bdk::max_ctas_per_sm(c->dev.G);
+  int bps = 1;
+  if (span > 0) {
+    bps = static_cast<int>(std::max<long>(1, ((long)cells * span + target - 1) / target));
+    bps = std::max(bps, (span + 255) / 256);
+  }
+  const int n_splits = span > 0 ? (span + bps - 1) / bps : 1;
+  const int ng = static_cast<int>(cfg->heads_q / cfg->heads_kv);
+  bdk_status s = ensure_workspace(c, n_splits + 1, ng);
+  if (s) return s;
+
+  bdk::DecodeArgs a;
+  a.q = static_cast<const __half*>(q);
+  a.k_new = static_cast<const __half*>(k_new);
+  a.v_new = static_cast<const __half*>(v_new);
+  a.out = out;
+  a.out_lse = lse;
+  a.part_o = c->part_o;
+  a.part_ml = c->part_ml;
+  a.heads_q = static_cast<int>(cfg->heads_q);
+  a.n_group = ng;
+  a.n_splits = n_splits;
+  a.blocks_per_split = bps;
+  a.blk_begin = lo;
+  a.blk_end = hi;
+  a.precise = c->precise;
+  a.sm_scale_log2 = (1.0f / std::sqrt(static_cast<float>(cfg->head_dim))) * bdk::kLog2e;
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(bdk::launch_decode(c->dev, a, stream), "decode launch");
+  if (k_new != nullptr) {  // mirror of the cache-update phase
+    for (int i = 0; i < cells; ++i) {
+      if (++c->res_len[i] == c->dev.G.n_r) {
+        c->res_len[i] = 0;
+        c->packed_blocks[i] += 1;
+      }
+    }
+  }
+  return BDK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bdk_last_error(void) { return g_err.c_str(); }
+
+const char* bdk_status_name(bdk_status s) {
+  switch (s) {
+    case BDK_OK: return "OK";
+    case BDK_CONFIG_ERROR: return "ConfigError";
+    case BDK_SHAPE_ERROR: return "ShapeError";
+    case BDK_UNSUPPORTED_BITS: return "UnsupportedBits";
+    case BDK_CODE_OVERFLOW: return "CodeOverflow";
+    case BDK_CAPACITY_ERROR: return "CapacityError";
+    case BDK_STATE_ERROR: return "StateError";
+    case BDK_FORMAT_ERROR: return "FormatError";
+    case BDK_EMPTY_INPUT: return "EmptyInput";
+    case BDK_CUDA_ERROR: return "CudaError";
+    case BDK_UNSUPPORTED: return "Unsupported";
+    case BDK_INVALID_ARGUMENT: return "InvalidArgument";
+  }
+  return "Unknown";
+}
+
+bdk_status bdk_validate_config(const bdk_attn_config* cfg) {
+  if (!cfg) return fail(BDK_INVALID_ARGUMENT, "null config");
+  return validate(cfg);
+}
+
+bdk_status bdk_cache_create(const bdk_cache_desc* d, bdk_cache** out) {
+  if (!d || !out) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (d->batch == 0 || d->heads_kv == 0 || d->head_dim == 0 || d->warp_n == 0)
+    return fail(BDK_CONFIG_ERROR, "cache geometry fields must be > 0");
+  if (d->num_bits != 2 && d->num_bits != 4 && d->num_bits != 8 && d->num_bits != 16)
+    return fail(BDK_UNSUPPORTED_BITS, "num_bits must be one of 2, 4, 8, 16");
+  if (d->k_axis > 1) return fail(BDK_CONFIG_ERROR, "k_axis must be 0 (KChannel) or 1 (KToken)");
+  const uint32_t pack = 16 / d->num_bits;
+  const uint32_t n_r = 8 * d->warp_n * pack;
+  if (d->num_bits != 16) {
+    if (d->group_size == 0 || d->head_dim % d->group_size != 0)
+      return fail(BDK_CONFIG_ERROR, "group_size must divide head_dim (token-wise V groups)");
+    if (d->k_axis == 0 && n_r % d->group_size != 0)
+      return fail(BDK_CONFIG_ERROR, "channel-wise group_size must divide N_r");
+  }
+  Geom G{};
+  G.batch = d->batch;
+  G.heads_kv = d->heads_kv;
+  G.d = d->head_dim;
+  G.warp_n = d->warp_n;
+  G.bits = d->num_bits;
+  G.k_axis = d->k_axis;
+  G.g = d->num_bits == 16 ? 1 : d->group_size;
+  G.interleave = d->interleave ? 1 : 0;
+  G.n_r = n_r;
+  G.pack = pack;
+  G.max_blocks = d->max_tokens / n_r + 1;
+  G.wbytes = d->head_dim * 16 * d->warp_n;
+  const uint32_t kp = param_u16(n_r, d->head_dim, d->num_bits, d->k_axis, G.g);
+  const uint32_t vp = param_u16(n_r, d->head_dim, d->num_bits, 1, G.g);
+  G.kp_bytes = 2 * kp;
+  G.vp_bytes = 2 * vp;
+  G.rec_bytes = ((2 * G.wbytes + G.kp_bytes + G.vp_bytes) + 127) / 128 * 128;
+  if (!bdk::fast_path_ok(G))
+    return fail(BDK_UNSUPPORTED,
+                "geometry outside the sm_100a kernel envelope (head_dim 128, warp_n in "
+                "{1,2,4,8}, group_size % 16 == 0, channel-wise group_size % (8*16/bits) == 0)");
+
+  bdk_cache* c = new bdk_cache();
+  c->desc = *d;
+  c->device = d->device;
+  c->kp_u16 = kp;
+  c->vp_u16 = vp;
+  c->wpb = d->head_dim * 8 * d->warp_n;
+  c->dev.G = G;
+  const size_t cells = (size_t)d->batch * d->heads_kv;
+  c->packed_blocks.assign(cells, 0);
+  c->res_len.assign(cells, 0);
+  cudaError_t e = cudaSetDevice(d->device);
+  if (e == cudaSuccess)
+    e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, d->device);
+  if (e == cudaSuccess)
+    e = cudaMalloc(&c->dev.records, cells * G.max_blocks * (size_t)G.rec_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->dev.res_k, cells * n_r * d->head_dim * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&c->dev.res_v, cells * n_r * d->head_dim * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&c->dev.packed_blocks, cells * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->dev.res_len, cells * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->dev.packed_blocks, 0, cells * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->dev.res_len, 0, cells * sizeof(int));
+  if (e != cudaSuccess) {
+    bdk_cache_destroy(c);
+    return cuda_fail(e, "bdk_cache_create");
+  }
+  *out = c;
+  return BDK_OK;
+}
+
+bdk_status bdk_cache_destroy(bdk_cache* c) {
+  if (!c) return BDK_OK;
+  cudaSetDevice(c->device);
+  cudaFree(c->dev.records);
+  cudaFree(c->dev.res_k);
+  cudaFree(c->dev.res_v);
+  cudaFree(c->dev.packed_blocks);
+  cudaFree(c->dev.res_len);
+  cudaFree(c->part_o);
+  cudaFree(c->part_ml);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  cudaFree(c->d_stage);
+  delete c;
+  return BDK_OK;
+}
+
+bdk_status bdk_cache_get_info(const bdk_cache* c, bdk_cache_info* info) {
+  if (!c || !info) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  info->n_r = c->dev.G.n_r;
+  info->pack_num = c->dev.G.pack;
+  info->words_per_block = c->wpb;
+  info->k_param_u16 = c->kp_u16;
+  info->v_param_u16 = c->vp_u16;
+  info->record_bytes = c->dev.G.rec_bytes;
+  info->max_blocks = c->dev.G.max_blocks;
+  info->fast_path = bdk::fast_path_ok(c->dev.G) ? 1 : 0;
+  return BDK_OK;
+}
+
+bdk_status bdk_cache_lengths(const bdk_cache* c, uint32_t b, uint32_t h, uint32_t* packed_len,
+                             uint32_t* res_len) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  const int i = cell_of(c, b, h);
+  if (packed_len) *packed_len = c->packed_blocks[i] * c->dev.G.n_r;
+  if (res_len) *res_len = c->res_len[i];
+  return BDK_OK;
+}
+
+bdk_status bdk_prefill(bdk_cache* c, uint32_t b, uint32_t h, const void* k, const void* v,
+                       uint32_t len, void* stream) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  const int i = cell_of(c, b, h);
+  if (c->packed_blocks[i] != 0 || c->res_len[i] != 0)
+    return fail(BDK_STATE_ERROR, "prefill into a non-empty cell");
+  const int nb = static_cast<int>(len / c->dev.G.n_r);
+  if (nb > c->dev.G.max_blocks) return fail(BDK_CAPACITY_ERROR, "prefill exceeds max_tokens");
+  if (len > 0 && (!k || !v)) return fail(BDK_INVALID_ARGUMENT, "null k/v");
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(bdk::launch_prefill(c->dev, static_cast<const __half*>(k),
+                               static_cast<const __half*>(v), static_cast<int>(len), i, 1,
+                               as_stream(stream)),
+           "prefill launch");
+  c->packed_blocks[i] = nb;
+  c->res_len[i] = static_cast<int>(len % c->dev.G.n_r);
+  return BDK_OK;
+}
+
+bdk_status bdk_prefill_all(bdk_cache* c, const void* k, const void* v, uint32_t len,
+                           void* stream) {
+  if (!c) return fail(BDK_INVALID_ARGUMENT, "null cache");
+  for (size_t i = 0; i < c->res_len.size(); ++i)
+    if (c->packed_blocks[i] != 0 || c->res_len[i] != 0)
+      return fail(BDK_STATE_ERROR, "prefill into a non-empty cell");
+  const int nb = static_cast<int>(len / c->dev.G.n_r);
+  if (nb > c->dev.G.max_blocks) return fail(BDK_CAPACITY_ERROR, "prefill exceeds max_tokens");
+  const int cells = static_cast<int>(c->res_len.size());
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(bdk::launch_prefill(c->dev, static_cast<const __half*>(k),
+                               static_cast<const __half*>(v), static_cast<int>(len), 0, cells,
+                               as_stream(stream)),
+           "prefill launch");
+  for (int i = 0; i < cells; ++i) {
+    c->packed_blocks[i] = nb;
+    c->res_len[i] = static_cast<int>(len % c->dev.G.n_r);
+  }
+  return BDK_OK;
+}
+
+bdk_status bdk_append_token(bdk_cache* c, uint32_t b, uint32_t h, const void* k, const void* v,
+                            void* stream) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  const int i = cell_of(c, b, h);
+  if (c->res_len[i] == c->dev.G.n_r)
+    return fail(BDK_CAPACITY_ERROR, "residual is full; flush before appending");
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(bdk::launch_append(c->dev, i, static_cast<const __half*>(k),
+                              static_cast<const __half*>(v), as_stream(stream)),
+           "append launch");
+  c->res_len[i] += 1;
+  return BDK_OK;
+}
+
+bdk_status bdk_flush_residual(bdk_cache* c, uint32_t b, uint32_t h, void* stream) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  const int i = cell_of(c, b, h);
+  if (c->res_len[i] != c->dev.G.n_r)
+    return fail(BDK_STATE_ERROR, "flush_residual requires res_len == N_r, have " +
+                                     std::to_string(c->res_len[i]));
+  if (c->packed_blocks[i] >= c->dev.G.max_blocks)
+    return fail(BDK_CAPACITY_ERROR, "cache arena full (raise max_tokens)");
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(bdk::launch_flush(c->dev, i, as_stream(stream)), "flush launch");
+  c->packed_blocks[i] += 1;
+  c->res_len[i] = 0;
+  return BDK_OK;
+}
+
+bdk_status bdk_decode_step(bdk_cache* c, const bdk_attn_config* cfg, const void* q,
+                           const void* k_new, const void* v_new, float* out, void* stream) {
+  bdk_status s = check_decode(c, cfg, true);
+  if (s) return s;
+  if (!q || !k_new || !v_new || !out) return fail(BDK_INVALID_ARGUMENT, "null tensor");
+  return run_decode(c, cfg, q, k_new, v_new, out, nullptr, 0, 1 << 30, as_stream(stream));
+}
+
+bdk_status bdk_decode_partial(bdk_cache* c, const bdk_attn_config* cfg, const void* q,
+                              const void* k_new, const void* v_new, uint32_t blk_begin,
+                              uint32_t blk_end, float* out, float* lse, void* stream) {
+  const bool appends = k_new != nullptr;
+  bdk_status s = check_decode(c, cfg, appends);
+  if (s) return s;
+  if (!q || !out || !lse || (appends && !v_new))
+    return fail(BDK_INVALID_ARGUMENT, "null tensor");
+  return run_decode(c, cfg, q, k_new, v_new, out, lse, static_cast<int>(blk_begin),
+                    static_cast<int>(std::min<uint32_t>(blk_end, 1u << 30)), as_stream(stream));
+}
+
+bdk_status bdk_merge_partials(const float* o, const float* lse, uint32_t n_parts, uint32_t rows,
+                              uint32_t d, float* out, void* stream) {
+  if (n_parts == 0) return fail(BDK_EMPTY_INPUT, "combine: no partial outputs");
+  if (!o || !lse || !out) return fail(BDK_INVALID_ARGUMENT, "null tensor");
+  BDK_CUDA(bdk::launch_merge_partials(o, lse, static_cast<int>(n_parts), static_cast<int>(rows),
+                                      static_cast<int>(d), out, as_stream(stream)),
+           "merge launch");
+  return BDK_OK;
+}
+
+bdk_status bdk_set_precise(bdk_cache* c, int precise) {
+  if (!c) return fail(BDK_INVALID_ARGUMENT, "null cache");
+  c->precise = precise ? 1 : 0;
+  return BDK_OK;
+}
+
+// host fp32 tensors -> fp16 on device (values are binary16-representable)
+namespace {
+__global__ void f32_to_f16_kernel(const float* in, __half* out, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    out[i] = __float2half_rn(in[i]);
+}
+}  // namespace
+
+bdk_status bdk_decode_step_host(bdk_cache* c, const bdk_attn_config* cfg, const float* q,
+                                const float* k_new, const float* v_new, float* out) {
+  bdk_status s = check_decode(c, cfg, true);
+  if (s) return s;
+  if (!q || !k_new || !v_new || !out) return fail(BDK_INVALID_ARGUMENT, "null tensor");
+  const size_t d = cfg->head_dim;
+  const size_t nq = (size_t)cfg->batch * cfg->heads_q * d;
+  const size_t nk = (size_t)cfg->batch * cfg->heads_kv * d;
+  const size_t n_in = nq + 2 * nk;
+  // layout of the staging buffers: fp32 in [q | k | v], fp16 [q | k | v], fp32 out
+  const size_t bytes = n_in * 4 + n_in * 2 + nq * 4 + 256;
+  s = ensure_stage(c, bytes);
+  if (s) return s;
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  float* hin = static_cast<float*>(c->h_stage);
+  std::memcpy(hin, q, nq * 4);
+  std::memcpy(hin + nq, k_new, nk * 4);
+  std::memcpy(hin + nq + nk, v_new, nk * 4);
+  float* din = static_cast<float*>(c->d_stage);
+  __half* dh = reinterpret_cast<__half*>(din + n_in);
+  float* dout = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(dh + n_in) + 127) & ~uintptr_t(127));
+  cudaStream_t st = 0;
+  BDK_CUDA(cudaMemcpyAsync(din, hin, n_in * 4, cudaMemcpyHostToDevice, st), "H2D");
+  f32_to_f16_kernel<<<static_cast<unsigned>(std::min<size_t>((n_in + 255) / 256, 1024)), 256, 0,
+                      st>>>(din, dh, n_in);
+  BDK_CUDA(cudaGetLastError(), "convert launch");
+  s = run_decode(c, cfg, dh, dh + nq, dh + nq + nk, dout, nullptr, 0, 1 << 30, st);
+  if (s) return s;
+  float* hout = hin + n_in;
+  BDK_CUDA(cudaMemcpyAsync(hout, dout, nq * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  BDK_CUDA(cudaStreamSynchronize(st), "decode_step_host");
+  std::memcpy(out, hout, nq * 4);
+  return BDK_OK;
+}
+
+bdk_status bdk_read_block(const bdk_cache* c, uint32_t b, uint32_t h, uint32_t blk,
+                          uint16_t* kw, uint16_t* vw, uint16_t* kp, uint16_t* vp) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  const int i = cell_of(c, b, h);
+  if (static_cast<int>(blk) >= c->packed_blocks[i])
+    return fail(BDK_SHAPE_ERROR, "block index past the packed segment");
+  const Geom& G = c->dev.G;
+  std::vector<uint8_t> rec(G.rec_bytes);
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(cudaDeviceSynchronize(), "sync");
+  BDK_CUDA(cudaMemcpy(rec.data(),
+                      c->dev.records + ((size_t)i * G.max_blocks + blk) * G.rec_bytes,
+                      G.rec_bytes, cudaMemcpyDeviceToHost),
+           "D2H block");
+  for (uint32_t w = 0; w < c->wpb; ++w) {  // undo the 16-byte chunk swizzle
+    const size_t off = word_offset(G, w);
+    if (kw) std::memcpy(kw + w, rec.data() + off, 2);
+    if (vw) std::memcpy(vw + w, rec.data() + G.wbytes + off, 2);
+  }
+  if (kp) std::memcpy(kp, rec.data() + 2 * G.wbytes, G.kp_bytes);
+  if (vp) std::memcpy(vp, rec.data() + 2 * G.wbytes + G.kp_bytes, G.vp_bytes);
+  return BDK_OK;
+}
+
+bdk_status bdk_adopt_block(bdk_cache* c, uint32_t b, uint32_t h, const uint16_t* kw,
+                           const uint16_t* vw, const uint16_t* kp, const uint16_t* vp) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  if (!kw || !vw || ((c->kp_u16 && !kp) || (c->vp_u16 && !vp)))
+    return fail(BDK_INVALID_ARGUMENT, "null block field");
+  const int i = cell_of(c, b, h);
+  const Geom& G = c->dev.G;
+  if (c->packed_blocks[i] >= G.max_blocks)
+    return fail(BDK_CAPACITY_ERROR, "cache arena full (raise max_tokens)");
+  std::vector<uint8_t> rec(G.rec_bytes, 0);
+  for (uint32_t w = 0; w < c->wpb; ++w) {
+    const size_t off = word_offset(G, w);
+    std::memcpy(rec.data() + off, kw + w, 2);
+    std::memcpy(rec.data() + G.wbytes + off, vw + w, 2);
+  }
+  if (G.kp_bytes) std::memcpy(rec.data() + 2 * G.wbytes, kp, G.kp_bytes);
+  if (G.vp_bytes) std::memcpy(rec.data() + 2 * G.wbytes + G.kp_bytes, vp, G.vp_bytes);
+  const int slot = c->packed_blocks[i];
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(cudaDeviceSynchronize(), "sync");
+  BDK_CUDA(cudaMemcpy(c->dev.records + ((size_t)i * G.max_blocks + slot) * G.rec_bytes,
+                      rec.data(), G.rec_bytes, cudaMemcpyHostToDevice),
+           "H2D block");
+  const int nb = slot + 1;
+  BDK_CUDA(cudaMemcpy(c->dev.packed_blocks + i, &nb, sizeof(int), cudaMemcpyHostToDevice),
+           "H2D length");
+  c->packed_blocks[i] = nb;
+  return BDK_OK;
+}
+
+bdk_status bdk_read_residual(const bdk_cache* c, uint32_t b, uint32_t h, uint16_t* k,
+                             uint16_t* v) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  const int i = cell_of(c, b, h);
+  const size_t n = (size_t)c->res_len[i] * c->desc.head_dim;
+  const size_t base = (size_t)i * c->dev.G.n_r * c->desc.head_dim;
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(cudaDeviceSynchronize(), "sync");
+  if (k && n) BDK_CUDA(cudaMemcpy(k, c->dev.res_k + base, n * 2, cudaMemcpyDeviceToHost), "D2H");
+  if (v && n) BDK_CUDA(cudaMemcpy(v, c->dev.res_v + base, n * 2, cudaMemcpyDeviceToHost), "D2H");
+  return BDK_OK;
+}
+
+bdk_status bdk_dequant_blocks(const bdk_cache* c, uint32_t b, uint32_t h, uint32_t blk0,
+                              uint32_t nblk, void* k_out, void* v_out, void* stream) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  const int i = cell_of(c, b, h);
+  if (static_cast<int>(blk0 + nblk) > c->packed_blocks[i])
+    return fail(BDK_SHAPE_ERROR, "packed_tile: range past packed segment");
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(bdk::launch_dequant(c->dev, i, static_cast<int>(blk0), static_cast<int>(nblk),
+                               static_cast<__half*>(k_out), static_cast<__half*>(v_out),
+                               as_stream(stream)),
+           "dequant launch");
+  return BDK_OK;
+}
+
+bdk_status bdk_memory(const bdk_cache* c, uint64_t out[4]) {
+  if (!c || !out) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  out[0] = out[1] = out[2] = out[3] = 0;
+  for (size_t i = 0; i < c->res_len.size(); ++i) {
+    out[0] += (uint64_t)c->packed_blocks[i] * c->wpb * 2;
+    out[1] += (uint64_t)c->packed_blocks[i] * c->wpb * 2;
+    out[2] += (uint64_t)c->packed_blocks[i] * (c->kp_u16 + c->vp_u16) * 2;
+    out[3] += (uint64_t)c->res_len[i] * c->desc.head_dim * 2 * 2;
+  }
+  return BDK_OK;
+}
+
+bdk_status bdk_corrupt_word(bdk_cache* c, uint32_t b, uint32_t h, uint32_t blk, uint32_t word,
+                            uint16_t value) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  const int i = cell_of(c, b, h);
+  if (static_cast<int>(blk) >= c->packed_blocks[i] || word >= c->wpb)
+    return fail(BDK_SHAPE_ERROR, "corrupt_word: index out of range");
+  const Geom& G = c->dev.G;
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(cudaDeviceSynchronize(), "sync");
+  BDK_CUDA(cudaMemcpy(c->dev.records + ((size_t)i * G.max_blocks + blk) * G.rec_bytes +
+                          word_offset(G, word),
+                      &value, 2, cudaMemcpyHostToDevice),
+           "H2D word");
+  return BDK_OK;
+}
+
+bdk_status bdk_synchronize(void) {
+  BDK_CUDA(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  return BDK_OK;
+}
+
+}  // extern "C"

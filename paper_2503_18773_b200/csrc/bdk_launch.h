@@ -1,0 +1,54 @@
+// bdk_launch.h -- host-side launchers for the sm_100a kernels (internal; the
+// public boundary is include/bitdecode_b200.h).
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bdk_common.cuh"
+
+namespace bdk {
+
+// Device state of one cache (owned by bdk_cache in bdk_api.cpp).
+struct DevCache {
+  Geom G;
+  uint8_t* records = nullptr;  // [cells][max_blocks][rec_bytes]
+  __half* res_k = nullptr;     // [cells][n_r][d]
+  __half* res_v = nullptr;
+  int* packed_blocks = nullptr;  // [cells]
+  int* res_len = nullptr;        // [cells]
+};
+
+struct DecodeArgs {
+  const __half* q = nullptr;      // [batch][heads_q][d]
+  const __half* k_new = nullptr;  // [batch][heads_kv][d] (nullptr: no append)
+  const __half* v_new = nullptr;
+  float* out = nullptr;           // [batch][heads_q][d] normalized output
+  float* out_lse = nullptr;       // optional [batch][heads_q] log2-sum-exp (partial mode)
+  float* part_o = nullptr;        // workspace [cells][n_parts][n_group][d]
+  float* part_ml = nullptr;       // workspace [cells][n_parts][n_group][2]
+  int heads_q = 0, n_group = 0;
+  int n_splits = 1, blocks_per_split = 1;
+  int blk_begin = 0, blk_end = 1 << 30;  // packed block range attended
+  int precise = 0;                        // hi/lo split P
+  float sm_scale_log2 = 0.f;
+};
+
+bool fast_path_ok(const Geom& G);
+int max_ctas_per_sm(const Geom& G);
+
+cudaError_t launch_prefill(const DevCache& c, const __half* k, const __half* v, int len,
+                           int cell_begin, int n_cells, cudaStream_t s);
+cudaError_t launch_append(const DevCache& c, int cell, const __half* k_row, const __half* v_row,
+                          cudaStream_t s);
+cudaError_t launch_flush(const DevCache& c, int cell, cudaStream_t s);
+cudaError_t launch_decode(const DevCache& c, const DecodeArgs& a, cudaStream_t s);
+// dequantize blocks [blk0, blk0+nblk) of a cell into fp16 [nblk*n_r][d] rows
+cudaError_t launch_dequant(const DevCache& c, int cell, int blk0, int nblk, __half* k_out,
+                           __half* v_out, cudaStream_t s);
+// merge normalized (o, lse) partials of n_parts ranks: o [n_parts][rows][d],
+// lse [n_parts][rows] (log2 domain) -> out [rows][d]
+cudaError_t launch_merge_partials(const float* o, const float* lse, int n_parts, int rows, int d,
+                                  float* out, cudaStream_t s);
+
+}  // namespace bdk

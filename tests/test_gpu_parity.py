@@ -1,0 +1,196 @@
+"""CUDA path vs the CPU oracle (bit-exact packing, decode within tolerance).
+
+Every call goes through the C-ABI (paper_2503_18773_b200/bitkv.py ->
+include/bitdecode_b200.h).  Tolerances (stated per DESIGN.md "Numerics"):
+  * packed words, params, residual bits, lengths: bit-exact
+  * decode, precise PV mode: max-abs < 1e-5 (the reference's own bar,
+    test_attention.cpp:350-441)
+  * decode, fast mode (fp16 P): max-abs < 2e-3 and rel-L2 < 1e-3
+"""
+import numpy as np
+import pytest
+
+from tests._cases import D, Case, errors, oracle_cache, prefill_data, step_data
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+FAST_TOL = {"max_abs": 2e-3, "rel_l2": 1e-3}
+PRECISE_TOL = {"max_abs": 1e-5}
+
+
+def _bk():
+    from paper_2503_18773_b200 import bitkv
+    return bitkv
+
+
+def gpu_cache(c: Case, k, v):
+    bk = _bk()
+    gc = bk.KVCache(c.batch, c.heads_kv, D, c.warp_n,
+                    bk.QuantSpec(c.bits, bk.QuantAxis(c.k_axis), c.group_size),
+                    interleave=c.interleave, max_tokens=c.prefill + c.steps + 2 * c.n_r)
+    gc.prefill_all(torch.from_numpy(k).cuda().half(), torch.from_numpy(v).cuda().half())
+    gc.set_precise(c.precise)
+    return gc
+
+
+def assert_same_cache(c: Case, gc, oc):
+    for b in range(c.batch):
+        for h in range(c.heads_kv):
+            assert gc.packed_len(b, h) == oc.packed_len(b, h)
+            assert gc.res_len(b, h) == oc.res_len(b, h)
+            for i in range(oc.packed_len(b, h) // oc.n_r):
+                got = gc.block(b, h, i)
+                kw, vw, kp, vp = oc.block(b, h, i)
+                assert np.array_equal(got.k_words, kw), (b, h, i, "k_words")
+                assert np.array_equal(got.v_words, vw), (b, h, i, "v_words")
+                assert np.array_equal(got.k_params, kp), (b, h, i, "k_params")
+                assert np.array_equal(got.v_params, vp), (b, h, i, "v_params")
+            rk, rv = gc.residual_tile(b, h)
+            ok_, ov_ = oc.residual(b, h)
+            assert np.array_equal(rk, ok_) and np.array_equal(rv, ov_)
+
+
+def run_decode(c: Case, check_blocks=True):
+    bk = _bk()
+    from oracle import oracle as O
+    g = O.Gauss(c.seed)
+    k, v = prefill_data(c, g)
+    oc = oracle_cache(c, k, v)
+    gc = gpu_cache(c, k, v)
+    if check_blocks:
+        assert_same_cache(c, gc, oc)
+    cfg = bk.AttentionConfig(batch=c.batch, heads_q=c.heads_q, heads_kv=c.heads_kv, head_dim=D,
+                             tile_m=max(1, c.heads_q // c.heads_kv), tile_n=8 * c.warp_n * 2,
+                             num_splits=4, warp_n=c.warp_n)
+    worst = {"max_abs": 0.0, "rel_l2": 0.0}
+    for _ in range(c.steps):
+        q, kn, vn = step_data(c, g)
+        ref = oc.decode_step(q, kn, vn, tile_n=cfg.tile_n, num_splits=4)
+        out = bk.decode_step(gc, cfg, torch.from_numpy(q).cuda().half(),
+                             torch.from_numpy(kn).cuda().half(),
+                             torch.from_numpy(vn).cuda().half())
+        got = out.data.cpu().numpy()
+        e = errors(got, ref)
+        worst = {kk: max(worst[kk], e[kk]) for kk in worst}
+    if check_blocks:
+        assert_same_cache(c, gc, oc)
+    return worst
+
+
+def check_tol(worst, precise):
+    tol = PRECISE_TOL if precise else FAST_TOL
+    for kk, lim in tol.items():
+        assert worst[kk] < lim, (worst, tol)
+
+
+# ------------------------------------------------------------------ packing
+@pytest.mark.parametrize("bits,warp_n,g,axis", [
+    (4, 4, 128, 0), (2, 4, 128, 0), (2, 2, 128, 0), (8, 2, 32, 0), (16, 4, 128, 0),
+    (4, 4, 64, 0), (4, 2, 32, 1), (2, 4, 64, 1), (4, 8, 128, 0), (8, 1, 16, 0)])
+def test_prefill_packs_bit_exact(bits, warp_n, g, axis):
+    from oracle import oracle as O
+    c = Case(bits=bits, warp_n=warp_n, group_size=g, k_axis=axis, heads_kv=2, batch=2,
+             prefill=3 * (8 * warp_n * (16 // bits)) + 37, seed=bits * 100 + warp_n)
+    gauss = O.Gauss(c.seed)
+    k, v = prefill_data(c, gauss)
+    assert_same_cache(c, gpu_cache(c, k, v), oracle_cache(c, k, v))
+
+
+def test_identity_permutation_packs_bit_exact():
+    from oracle import oracle as O
+    c = Case(bits=4, warp_n=4, heads_kv=2, prefill=300, interleave=False, seed=9)
+    k, v = prefill_data(c, O.Gauss(c.seed))
+    assert_same_cache(c, gpu_cache(c, k, v), oracle_cache(c, k, v))
+
+
+def test_zero_extremes_keep_the_reference_sign():
+    """min/max == +-0 keep the first element's sign (quant.cpp:20-23)."""
+    from oracle import oracle as O
+    c = Case(bits=4, warp_n=4, heads_kv=1, prefill=128, seed=3)
+    k, v = prefill_data(c, O.Gauss(c.seed))
+    k[0, 0, :, 5] = np.abs(k[0, 0, :, 5])
+    k[0, 0, 7, 5] = -0.0
+    k[0, 0, 9, 5] = 0.0
+    v[0, 0, 3, :] = np.abs(v[0, 0, 3, :])
+    v[0, 0, 3, 17] = 0.0
+    v[0, 0, 3, 40] = -0.0
+    v[0, 0, 4, :] = -np.abs(v[0, 0, 4, :])
+    v[0, 0, 4, 2] = -0.0
+    v[0, 0, 4, 90] = 0.0
+    assert_same_cache(c, gpu_cache(c, k, v), oracle_cache(c, k, v))
+
+
+# ------------------------------------------------------------------- decode
+@pytest.mark.parametrize("bits,warp_n", [(4, 4), (2, 4), (2, 2), (8, 2), (16, 4), (4, 8),
+                                         (4, 1)])
+def test_decode_matches_oracle(bits, warp_n):
+    n_r = 8 * warp_n * (16 // bits)
+    c = Case(bits=bits, warp_n=warp_n, heads_kv=4, heads_q=16, batch=2,
+             prefill=5 * n_r + n_r - 3, steps=5, seed=bits + 7 * warp_n,
+             group_size=min(128, n_r))
+    check_tol(run_decode(c), False)
+
+
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (32, 32), (8, 1), (8, 8), (16, 8)])
+def test_decode_gqa_groupings(hq, hkv):
+    c = Case(bits=4, warp_n=4, heads_q=hq, heads_kv=hkv, batch=1, prefill=700, steps=2,
+             seed=hq * 3 + hkv)
+    check_tol(run_decode(c), False)
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8, 16])
+def test_decode_precise_mode_meets_reference_tolerance(bits):
+    c = Case(bits=bits, warp_n=4, heads_kv=2, heads_q=8, batch=1, prefill=900, steps=3,
+             seed=50 + bits, precise=True, group_size=128 if bits != 8 else 64)
+    check_tol(run_decode(c), True)
+
+
+def test_decode_k_token_axis_and_small_groups():
+    c = Case(bits=4, warp_n=4, k_axis=1, group_size=32, heads_kv=2, heads_q=8, prefill=640,
+             steps=3, seed=77)
+    check_tol(run_decode(c), False)
+
+
+def test_residual_flush_happens_on_the_nth_step():
+    """test_attention.cpp:401-421: the N_r-th step flushes exactly once."""
+    bk = _bk()
+    c = Case(bits=4, warp_n=1, heads_kv=1, heads_q=1, batch=1, prefill=0, steps=0,
+             group_size=32, seed=8)
+    gc = gpu_cache(c, np.zeros((1, 1, 0, D), np.float32), np.zeros((1, 1, 0, D), np.float32))
+    from oracle import oracle as O
+    g = O.Gauss(8)
+    cfg = bk.AttentionConfig(batch=1, heads_q=1, heads_kv=1, head_dim=D, tile_n=8, warp_n=1)
+    n_r = gc.n_r()
+    for s in range(n_r - 1):
+        q, kn, vn = step_data(c, g)
+        bk.decode_step(gc, cfg, torch.from_numpy(q).cuda().half(),
+                       torch.from_numpy(kn).cuda().half(), torch.from_numpy(vn).cuda().half())
+        assert gc.packed_len(0, 0) == 0 and gc.res_len(0, 0) == s + 1
+    q, kn, vn = step_data(c, g)
+    bk.decode_step(gc, cfg, torch.from_numpy(q).cuda().half(),
+                   torch.from_numpy(kn).cuda().half(), torch.from_numpy(vn).cuda().half())
+    assert gc.packed_len(0, 0) == n_r and gc.res_len(0, 0) == 0
+
+
+def test_long_context_c1_shape():
+    """BASELINE configs[0] shape (LLaMA-3.1-8B, 4K, 4-bit g128 N_r 128)."""
+    c = Case(bits=4, warp_n=4, heads_q=32, heads_kv=8, batch=1, prefill=4096, steps=3, seed=1)
+    check_tol(run_decode(c), False)
+
+
+def test_host_api_matches_device_api():
+    """bdk_decode_step_host (host fp32 in/out) == device path."""
+    bk = _bk()
+    from oracle import oracle as O
+    c = Case(bits=4, warp_n=4, heads_q=8, heads_kv=2, prefill=500, steps=1, seed=4)
+    g = O.Gauss(c.seed)
+    k, v = prefill_data(c, g)
+    a, b_ = gpu_cache(c, k, v), gpu_cache(c, k, v)
+    cfg = bk.AttentionConfig(batch=1, heads_q=8, heads_kv=2, head_dim=D, warp_n=4)
+    q, kn, vn = step_data(c, g)
+    oh = bk.decode_step(a, cfg, q, kn, vn).data
+    od = bk.decode_step(b_, cfg, torch.from_numpy(q).cuda().half(),
+                        torch.from_numpy(kn).cuda().half(),
+                        torch.from_numpy(vn).cuda().half()).data.cpu().numpy()
+    assert np.array_equal(oh, od)
