@@ -1,0 +1,459 @@
+"""bench.py -- BitDecoding decode hot path on B200: quantized-KV decode attention.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2|C5|C3|C1]
+                    [--impl ours|reference] [--no-cpu-baseline] [--extra]
+
+Prints ONE JSON line (rank 0).  The metric is BASELINE.json's: decode-attention
+latency and HBM GB/s on quantized-KV bytes.  ``value`` = quantized-KV bytes
+read per step (KVCache::memory() payload + params, kvcache.cpp:330-345; the
+SURVEY.md 8(d) model) summed over all ranks / max-over-ranks device time of the
+K timed steps.  A "step" is one ``decode_step`` (attention.cpp:164-242) of the
+whole batch: append of the new token, residual + split-KV packed attention,
+LSE combine, commit (a full residual is quantized+packed inside the step).
+
+Default workload (N=1): BASELINE.json configs[1] = C2, LLaMA-3.1-8B GQA
+(32 q / 8 KV heads, d 128), 2-bit KV (KChannel K, group 128, W_n 4 -> N_r 256),
+batch 8, 32K context.  L2: every workload rotates across >= 2 cache replicas
+whose combined quantized bytes exceed 2x L2, so each step reads its replica
+from HBM (no flush kernel inside the timed region).
+
+--gpus N > 1 (torchrun, one process per GPU, NCCL): C2/C3/C1 are weak-scaled
+(each rank owns its own batch of sequences; no data-path collective).  C5 is
+sequence-split (strong scaling): each rank attends a contiguous block range of
+the 128K context and the normalized (o, lse) partials are all-gathered over
+NCCL and LSE-merged (combine, attention.cpp:142-162).
+
+--impl reference: the reference's own CPU engine (oracle/_ref, the unmodified
+/root/reference/proj sources compiled out-of-tree) timed through its own
+run_bench (bench.cpp:80-210) on this host's cores, same workload and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+D = 128
+WORKLOADS = {
+    "C1": dict(batch=1, hq=32, hkv=8, bits=4, warp_n=4, g=128, seq=4096,
+               desc="LLaMA-3.1-8B decode attn, b1, 32q/8kv, d128, 4-bit g128 N_r128, 4K"),
+    "C2": dict(batch=8, hq=32, hkv=8, bits=2, warp_n=4, g=128, seq=32768,
+               desc="LLaMA-3.1-8B decode attn, b8, 32q/8kv, d128, 2-bit g128 N_r256, 32K"),
+    "C3": dict(batch=32, hq=32, hkv=32, bits=4, warp_n=4, g=128, seq=8192,
+               desc="LLaMA-2-7B MHA decode attn, b32, 32q/32kv, d128, 4-bit g128 N_r128, 8K"),
+    "C5": dict(batch=1, hq=32, hkv=8, bits=4, warp_n=4, g=128, seq=131072,
+               desc="LLaMA-3.1-8B decode attn, b1, 32q/8kv, d128, 4-bit g128 N_r128, 128K"),
+}
+METRIC = ("decode-attn latency (µs) & HBM GB/s on quantized KV vs 8 TB/s, 4/2-bit, "
+          "32K–128K")
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        for k in ("hbm_gbs", "hbm_GBps", "hbm_copy_gbs"):
+            if k in j:
+                return float(j[k]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        pass
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+def qbytes_model(w, seq=None):
+    """packed payload + params bytes of all cells."""
+    n_r = 8 * w["warp_n"] * (16 // w["bits"])
+    seq = w["seq"] if seq is None else seq
+    plen = seq - seq % n_r
+    cells = w["batch"] * w["hkv"]
+    return cells * (2 * plen * D * w["bits"] // 8 + 4 * D * plen // w["g"] + 4 * plen * D // w["g"])
+
+
+# ----------------------------------------------------------------- dist
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Clocks:
+    """nvidia-smi clock / throttle sampling during the measured region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# -------------------------------------------------------------- our arm
+def run_ours(args, w, world, rank, local):
+    import torch
+    import torch.distributed as dist
+    from paper_2503_18773_b200 import bitkv as bk
+    from paper_2503_18773_b200 import sharding
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    seq_split = args.workload == "C5" and world > 1
+    props = torch.cuda.get_device_properties(dev)
+    l2 = getattr(props, "L2_cache_size", 126 * 2**20)
+    spec = bk.QuantSpec(w["bits"], bk.QuantAxis.KChannel, w["g"])
+    n_r = bk.residual_block_size(w["bits"], w["warp_n"])
+    cfg = bk.AttentionConfig(batch=w["batch"], heads_q=w["hq"], heads_kv=w["hkv"], head_dim=D,
+                             tile_m=max(1, w["hq"] // w["hkv"]), tile_n=64, num_splits=4,
+                             warp_n=w["warp_n"])
+    # sequence split: this rank's block range of the prefilled context
+    if seq_split:
+        nblk = w["seq"] // n_r
+        blk_lo, blk_hi = sharding.block_range(nblk, world, rank)
+        local_seq = (blk_hi - blk_lo) * n_r + (w["seq"] % n_r if rank == world - 1 else 0)
+    else:
+        local_seq = w["seq"]
+    per_rep = qbytes_model(w, local_seq)
+    n_rep = max(2, -(-2 * l2 // max(per_rep, 1)))
+    headroom = args.warmup + args.steps + args.e2e_steps + 2 * n_r
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    reps = []
+    t_pref = []
+    for _ in range(n_rep):
+        c = bk.KVCache(w["batch"], w["hkv"], D, w["warp_n"], spec, max_tokens=local_seq + headroom,
+                       device=local)
+        k = torch.randn((w["batch"], w["hkv"], local_seq, D), generator=gen, device=dev,
+                        dtype=torch.float16)
+        v = torch.randn((w["batch"], w["hkv"], local_seq, D), generator=gen, device=dev,
+                        dtype=torch.float16)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        c.prefill_all(k, v)
+        e1.record()
+        torch.cuda.synchronize()
+        t_pref.append(e0.elapsed_time(e1))
+        del k, v
+        reps.append(c)
+    torch.cuda.empty_cache()
+    K, W = args.steps, args.warmup
+    qs = torch.randn((K + W, w["batch"], w["hq"], D), generator=gen, device=dev).half()
+    kns = torch.randn((K + W, w["batch"], w["hkv"], D), generator=gen, device=dev).half()
+    vns = torch.randn((K + W, w["batch"], w["hkv"], D), generator=gen, device=dev).half()
+    q = torch.empty_like(qs[0])
+    kn = torch.empty_like(kns[0])
+    vn = torch.empty_like(vns[0])
+    out = torch.empty((w["batch"], w["hq"], D), device=dev, dtype=torch.float32)
+    lse = torch.empty((w["batch"], w["hq"]), device=dev, dtype=torch.float32)
+    steppers = [bk.DecodeStepper(c, cfg, q, kn, vn, out) for c in reps]
+    comm = sharding.SeqSplitComm(world, w["batch"] * w["hq"], D, dev) if seq_split else None
+
+    def one_step(i):
+        r = reps[i % n_rep]
+        q.copy_(qs[i])
+        kn.copy_(kns[i])
+        vn.copy_(vns[i])
+        if seq_split:
+            last = rank == world - 1
+            bk.decode_partial(r, cfg, q, kn if last else None, vn if last else None,
+                              0, 1 << 30, out=comm.o, lse=comm.lse)
+            comm.merge(out)
+        else:
+            steppers[i % n_rep]()
+        return sum(r.memory().__dict__[f] for f in
+                   ("k_packed_payload_bytes", "v_packed_payload_bytes", "params_bytes"))
+
+    # soak (untimed, no append): keeps clocks up while nvidia-smi samples
+    clocks = Clocks(local)
+    clocks.start()
+    t_end = time.time() + args.soak
+    while time.time() < t_end:
+        for r in reps:
+            bk.decode_partial(r, cfg, q, None, None, 0, 1 << 30, out=out, lse=lse)
+        torch.cuda.synchronize()
+    for i in range(W):
+        one_step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for r in reps:
+        r.profile_begin()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    bytes_total = 0
+    ev0.record()
+    for i in range(W, W + K):
+        bytes_total += one_step(i)
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    kern_ms, launches = 0.0, 0
+    for r in reps:
+        a, b = r.profile_end()
+        kern_ms += a
+        launches += b
+
+    # e2e through the public host API (host fp32 in, host fp32 out; copies inside)
+    import numpy as np
+    e2e_ms = None
+    h2d = d2h = 0
+    if not seq_split and args.e2e_steps > 0:
+        hq = np.random.default_rng(rank).standard_normal(
+            (args.e2e_steps, w["batch"], w["hq"], D)).astype(np.float16).astype(np.float32)
+        hk = np.random.default_rng(rank + 1).standard_normal(
+            (args.e2e_steps, w["batch"], w["hkv"], D)).astype(np.float16).astype(np.float32)
+        hv = np.random.default_rng(rank + 2).standard_normal(
+            (args.e2e_steps, w["batch"], w["hkv"], D)).astype(np.float16).astype(np.float32)
+        bk.decode_step(reps[0], cfg, hq[0], hk[0], hv[0])  # staging allocation
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e2e_bytes = 0
+        t0 = time.perf_counter()
+        for i in range(args.e2e_steps):
+            r = reps[i % n_rep]
+            res = bk.decode_step(r, cfg, hq[i], hk[i], hv[i])
+            e2e_bytes += sum(r.memory().__dict__[f] for f in
+                             ("k_packed_payload_bytes", "v_packed_payload_bytes",
+                              "params_bytes"))
+        e2e_ms = (time.perf_counter() - t0) * 1e3
+        assert np.isfinite(res.data).all()
+        h2d = (hq[0].size + hk[0].size + hv[0].size) * 4
+        d2h = hq[0].size * 4
+
+    # max over ranks, sum of bytes
+    t = torch.tensor([ms, e2e_ms or 0.0, kern_ms], dtype=torch.float64, device=dev)
+    b = torch.tensor([float(bytes_total)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if not seq_split:
+            dist.all_reduce(b, op=dist.ReduceOp.SUM)
+    ms, e2e_ms_max, _ = t.tolist()
+    total_bytes = b.item() if not seq_split else qbytes_model(w) * K
+    if rank != 0:
+        return None
+    gbs = total_bytes / (ms * 1e-3) / 1e9
+    peak, peak_src = peak_hbm()
+    per_launch_bytes = bytes_total / max(launches, 1)
+    kern_avg_ms = kern_ms / max(launches, 1)
+    achieved = per_launch_bytes / (kern_avg_ms * 1e-3) / 1e9 if launches else None
+    res = {
+        "metric": METRIC, "value": round(gbs, 1), "unit": "GB/s", "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": round(ms / K, 5),
+        "latency_us": round(ms / K * 1e3, 2), "higher_is_better": True,
+        "scaling": "strong" if seq_split else "weak", "vs_baseline": None,
+        "dtype": f"u{w['bits']} codes -> fp16 MMA, fp32 accumulate", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {w['desc']}", "batch_per_gpu": w["batch"],
+                   "global_batch": w["batch"] * (1 if seq_split else world),
+                   "seq_len": w["seq"], "bits": w["bits"], "group_size": w["g"],
+                   "warp_n": w["warp_n"], "n_r": n_r,
+                   "parallelism": (f"seq-split{world} (NCCL all-gather of (o,lse))" if seq_split
+                                   else (f"dp{world} (independent batches)" if world > 1
+                                         else "single GPU")),
+                   "l2": f"rotating {n_rep} cache replicas x {per_rep/1e6:.1f} MB quantized "
+                         f"(> 2x L2 {l2/2**20:.0f} MiB); inputs larger than L2, no flush",
+                   "quantized_bytes_per_step": round(total_bytes / K)},
+        "roofline": {"bound": "hbm",
+                     "achieved": round(achieved, 1) if achieved else None,
+                     "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4) if achieved else None,
+                     "peak_source": peak_src,
+                     "kernel": "bdk::decode_kernel (split-KV attention over packed blocks)",
+                     "kernel_avg_us": round(kern_avg_ms * 1e3, 2),
+                     "kernel_share_of_step": round(kern_ms / ms, 3) if ms else None,
+                     "algorithmic_bytes_per_launch": round(per_launch_bytes),
+                     "traffic": load_traffic(args.workload)},
+        "e2e": ({"value": round(e2e_bytes_rate(bytes_total / K, args.e2e_steps, e2e_ms_max,
+                                               world), 2),
+                 "unit": "GB/s", "latency_us": round(e2e_ms_max / args.e2e_steps * 1e3, 1),
+                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                 "path": "bitkv.decode_step(host fp32 arrays) -> bdk_decode_step_host "
+                         "(pinned staging, H2D, fp16 convert, decode, D2H, sync)",
+                 "clock": "host perf_counter (synchronous call)"}
+                if e2e_ms else None),
+        "gpu_launches": (launches * 2) if not seq_split else launches * 2 + K,
+        "clocks": clk,
+        "prefill_ms_per_replica": round(statistics.median(t_pref), 3),
+    }
+    return res
+
+
+def e2e_bytes_rate(bytes_per_step, steps, ms, world):
+    return bytes_per_step * world * steps / (ms * 1e-3) / 1e9
+
+
+def load_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_decode_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------- CPU reference arm
+def cpu_reference(w, steps, warm=1):
+    """The unmodified reference engine (oracle/_ref) via its own run_bench,
+    or the C restatement (kind "port") when _ref is absent.  Returns
+    (GB/s, mean step ms, kind, cores, sample)."""
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    os.environ["BITKV_THREADS"] = str(cores)
+    n_r = 8 * w["warp_n"] * (16 // w["bits"])
+    qb = qbytes_model(w)
+    if O.have_ref():
+        r = O.ref_run_bench(mode=1 if w["batch"] > 1 else 0, seq_len=w["seq"], batch=w["batch"],
+                            heads_q=w["hq"], heads_kv=w["hkv"], head_dim=D, bits=w["bits"],
+                            group_size=w["g"], k_axis=0, num_splits=4, steps=warm + steps,
+                            seed=0, tile_n=64, warp_n=w["warp_n"])
+        mem = r["memory"]
+        qb = mem[0] + mem[1] + mem[2]
+        st = r["step_ms"][warm:]
+        ms = sum(st) / len(st)
+        kind = "reference"
+        sample = (f"reference run_bench (bench.cpp:80-210), full {w['seq']}-token shape, "
+                  f"{steps} timed decode steps after {warm} warm-up, prefill "
+                  f"{r['prefill_seconds']:.2f} s single-threaded; BITKV_THREADS={cores}")
+    else:
+        import numpy as np
+        g = O.Gauss(0)
+        oc = O.OracleCache(w["batch"], w["hkv"], D, w["warp_n"], w["bits"], 0, w["g"], True,
+                           max_tokens=w["seq"] + steps + warm + n_r)
+        for b in range(w["batch"]):
+            for h in range(w["hkv"]):
+                k = g.rounded(w["seq"] * D).reshape(w["seq"], D)
+                v = g.rounded(w["seq"] * D).reshape(w["seq"], D)
+                oc.prefill(b, h, k, v)
+        times = []
+        for s in range(warm + steps):
+            q = g.rounded(w["batch"] * w["hq"] * D).reshape(w["batch"], w["hq"], D)
+            kn = g.rounded(w["batch"] * w["hkv"] * D).reshape(w["batch"], w["hkv"], D)
+            vn = g.rounded(w["batch"] * w["hkv"] * D).reshape(w["batch"], w["hkv"], D)
+            t0 = time.perf_counter()
+            oc.decode_step(q, kn, vn, threads=cores)
+            times.append((time.perf_counter() - t0) * 1e3)
+        ms = sum(times[warm:]) / steps
+        kind = "port"
+        sample = (f"oracle C restatement (oracle/bitkv_oracle.c), full shape, {steps} steps, "
+                  f"{cores} threads")
+        del np
+    return qb / (ms * 1e-3) / 1e9, ms, kind, cores, sample
+
+
+def run_reference_arm(args, w, world, rank):
+    if rank != 0:
+        return None
+    steps = args.steps
+    # bound the run: the reference step at C2/C5 is ~1 s on 8 cores
+    est = {"C1": 0.05, "C2": 1.7, "C3": 5.0, "C5": 0.9}[args.workload] * 8 / (os.cpu_count() or 8)
+    cap = max(2, int(150 / max(est, 1e-3)))
+    k_run = min(steps, cap)
+    gbs, ms, kind, cores, sample = cpu_reference(w, k_run, warm=min(args.warmup, 1))
+    if k_run < steps:
+        sample += f" (K capped at {k_run} of {steps} to bound the run)"
+    line = {"impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s",
+            "n_gpus": world, "steps": k_run, "warmup": min(args.warmup, 1),
+            "ms_per_step": round(ms, 3), "latency_us": round(ms * 1e3, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": f"u{w['bits']} codes -> fp32 (CPU)", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {w['desc']}", "global_batch": w["batch"],
+                       "seq_len": w["seq"]},
+            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores,
+                             "kind": kind, "sample": sample},
+            "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--soak", type=float, default=1.0, help="untimed seconds before timing")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    w = WORKLOADS[args.workload]
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        line = run_reference_arm(args, w, world, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        res = run_ours(args, w, world, rank, local)
+        if res is not None:
+            if world == 1 and not args.no_cpu_baseline:
+                gbs, ms, kind, cores, sample = cpu_reference(w, args.cpu_steps)
+                res["cpu_baseline"] = {"value": round(gbs, 4), "unit": "GB/s", "cores": cores,
+                                       "kind": kind, "sample": sample,
+                                       "ms_per_step": round(ms, 2)}
+            else:
+                res["cpu_baseline"] = None
+            print(json.dumps(res), flush=True)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

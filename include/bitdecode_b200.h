@@ -149,9 +149,13 @@ BDK_API bdk_status bdk_decode_partial(bdk_cache* cache, const bdk_attn_config* c
                                       const void* v_new_dev, uint32_t blk_begin,
                                       uint32_t blk_end, float* out_dev, float* lse_dev,
                                       void* stream);
-/* o_dev [n_parts][rows][d], lse_dev [n_parts][rows] -> out_dev [rows][d] */
+/* LSE merge of n_parts normalized partials: part p is o_dev + p*o_stride
+ * ([rows][d] fp32) and lse_dev + p*lse_stride ([rows], log2 domain), strides
+ * in floats (so one all-gathered [n_parts][rows*d + rows] buffer merges in
+ * place) -> out_dev [rows][d]. */
 BDK_API bdk_status bdk_merge_partials(const float* o_dev, const float* lse_dev, uint32_t n_parts,
-                                      uint32_t rows, uint32_t d, float* out_dev, void* stream);
+                                      uint32_t rows, uint32_t d, uint64_t o_stride,
+                                      uint64_t lse_stride, float* out_dev, void* stream);
 /* 0 = fast (fp16 P), 1 = precise PV (P = P_hi + P_lo) */
 BDK_API bdk_status bdk_set_precise(bdk_cache* cache, int precise);
 
@@ -182,6 +186,13 @@ BDK_API bdk_status bdk_memory(const bdk_cache* cache, uint64_t out[4]);
 /* KVCache::corrupt_word (kvcache.cpp:326-328): fault injection on K words. */
 BDK_API bdk_status bdk_corrupt_word(bdk_cache* cache, uint32_t b, uint32_t h, uint32_t blk,
                                     uint32_t word, uint16_t value);
+/* Attention-kernel timing: between begin and end every decode launch of the
+ * cache records a CUDA event pair on its launching stream immediately around
+ * the split-KV attention kernel.  end synchronizes on the events and returns
+ * the summed kernel time and the number of launches (measurement hook for
+ * bench.py's roofline; no reference counterpart). */
+BDK_API bdk_status bdk_profile_begin(bdk_cache* cache);
+BDK_API bdk_status bdk_profile_end(bdk_cache* cache, float* total_ms, uint32_t* launches);
 /* Blocks until all work on the cache's device is done; reports async errors. */
 BDK_API bdk_status bdk_synchronize(void);
 

@@ -370,7 +370,8 @@ class Reference:
             L.ref_naive_attention.argtypes = [_f32p, _sz, _f32p, _f32p, _sz, _sz, _f32p]
             L.ref_run_bench.argtypes = [C.c_int, _sz, _sz, _sz, _sz, _sz, C.c_uint32, _sz,
                                         C.c_uint32, _sz, _sz, C.c_uint64, _sz, _sz, C.c_int,
-                                        C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+                                        C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                        C.POINTER(C.c_double), _sz]
             L.ref_run_verify.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32]
             cls._lib = L
         return cls._lib
@@ -508,15 +509,17 @@ def ref_run_bench(*, mode=0, seq_len=4096, batch=1, heads_q=32, heads_kv=8, head
     """The reference's own run_bench (bench.cpp:80-210)."""
     out = (C.c_double * 11)()
     orc = (C.c_double * 3)()
+    step_ms = (C.c_double * max(1, steps))()
     _rcheck(Reference.lib().ref_run_bench(mode, seq_len, batch, heads_q, heads_kv, head_dim, bits,
                                           group_size, k_axis, num_splits, steps, seed, tile_n,
-                                          warp_n, int(interleave), int(verify), out, orc),
+                                          warp_n, int(interleave), int(verify), out, orc,
+                                          step_ms, steps),
             "run_bench")
     ck = np.array([out[5]], np.float64).view(np.uint64)[0]
     return {"prefill_seconds": out[0], "mean_ms": out[1], "p50_ms": out[2], "p99_ms": out[3],
             "tokens_per_second": out[4], "output_checksum": int(ck),
             "memory": [int(out[6]), int(out[7]), int(out[8]), int(out[9])], "n_r": int(out[10]),
-            "oracle": list(orc)}
+            "oracle": list(orc), "step_ms": list(step_ms)[:steps]}
 
 
 def ref_run_verify(seed_begin=0, seed_end=2, bits=4) -> int:

@@ -13,6 +13,7 @@
 #include <exception>
 #include <sstream>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "bitkv/attention.hpp"
@@ -204,7 +205,8 @@ void ref_naive_attention(const float* q, size_t rows, const float* k, const floa
 int ref_run_bench(int mode, size_t seq_len, size_t batch, size_t heads_q, size_t heads_kv,
                   size_t head_dim, uint32_t bits, size_t group_size, uint32_t k_axis,
                   size_t num_splits, size_t steps, uint64_t seed, size_t tile_n, size_t warp_n,
-                  int interleave, int verify, double* out, double* oracle3) {
+                  int interleave, int verify, double* out, double* oracle3, double* step_ms,
+                  size_t step_cap) {
   GUARD({
     WorkloadSpec s;
     s.mode = mode == 0 ? WorkloadMode::Single
@@ -236,6 +238,8 @@ int ref_run_bench(int mode, size_t seq_len, size_t batch, size_t heads_q, size_t
     out[8] = double(r.memory.params_bytes);
     out[9] = double(r.memory.residual_bytes);
     out[10] = double(r.n_r);
+    for (size_t i = 0; step_ms && i < std::min(step_cap, r.step_seconds.size()); ++i)
+      step_ms[i] = r.step_seconds[i] * 1e3;
     if (oracle3) {
       oracle3[0] = r.oracle.max_abs_err;
       oracle3[1] = r.oracle.rel_l2_err;

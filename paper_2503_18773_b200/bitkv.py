@@ -373,6 +373,16 @@ class KVCache:
         _check(_L.load().bdk_memory(self._h, out))
         return Memory(*[int(x) for x in out])
 
+    def profile_begin(self) -> None:
+        """Start CUDA-event timing of the attention kernel (bdk_profile_begin)."""
+        _check(_L.load().bdk_profile_begin(self._h))
+
+    def profile_end(self) -> tuple[float, int]:
+        """(summed attention-kernel ms, launches) since profile_begin."""
+        ms, n = C.c_float(), C.c_uint32()
+        _check(_L.load().bdk_profile_end(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
     def set_precise(self, precise: bool) -> None:
         """fp16 P (False) or P_hi + P_lo split PV (True), SURVEY.md F4."""
         _check(_L.load().bdk_set_precise(self._h, 1 if precise else 0))
@@ -427,17 +437,44 @@ def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None)
     return AttnOutput(cfg.batch, cfg.heads_q, cfg.head_dim, out)
 
 
+class DecodeStepper:
+    """Pointer-bound ``decode_step`` for steady-state loops: the C-ABI call
+    with arguments prepared once (q/k_new/v_new/out are CUDA tensors whose
+    storage stays fixed; refill them in place between steps).  Same kernels
+    and semantics as :func:`decode_step`."""
+
+    def __init__(self, cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out):
+        for t in (q, k_new, v_new):
+            if not (t.is_cuda and t.dtype == torch.float16 and t.is_contiguous()):
+                raise ShapeError("DecodeStepper needs contiguous CUDA fp16 q/k_new/v_new")
+        if not (out.is_cuda and out.dtype == torch.float32 and out.is_contiguous()):
+            raise ShapeError("DecodeStepper needs a contiguous CUDA fp32 out")
+        self._cfg = cfg._c()
+        self._fn = _L.load().bdk_decode_step
+        self._args = (cache.handle(), C.byref(self._cfg), C.c_void_p(q.data_ptr()),
+                      C.c_void_p(k_new.data_ptr()), C.c_void_p(v_new.data_ptr()),
+                      C.c_void_p(out.data_ptr()))
+        self._keep = (cache, q, k_new, v_new, out)
+
+    def __call__(self, stream=None) -> None:
+        st = self._fn(*self._args, stream if stream is not None else _stream_ptr())
+        if st:
+            _check(st)
+
+
 def decode_partial(cache: KVCache, cfg: AttentionConfig, q, k_new=None, v_new=None,
-                   blk_begin: int = 0, blk_end: int = 1 << 30):
+                   blk_begin: int = 0, blk_end: int = 1 << 30, out=None, lse=None):
     """Sequence-split partial (see bdk_decode_partial): returns the normalized
-    partial output [batch, heads_q, d] and its log2-sum-exp [batch, heads_q]."""
+    partial output [batch, heads_q, d] and its log2-sum-exp [batch, heads_q].
+    k_new/v_new None: attend only (no append, no commit)."""
     c = cfg._c()
     qd = _as_f16_cuda(q)
     kd = _as_f16_cuda(k_new) if k_new is not None else None
     vd = _as_f16_cuda(v_new) if v_new is not None else None
-    o = torch.empty((cfg.batch, cfg.heads_q, cfg.head_dim), dtype=torch.float32,
-                    device=qd.device)
-    lse = torch.empty((cfg.batch, cfg.heads_q), dtype=torch.float32, device=qd.device)
+    o = out if out is not None else torch.empty((cfg.batch, cfg.heads_q, cfg.head_dim),
+                                                dtype=torch.float32, device=qd.device)
+    if lse is None:
+        lse = torch.empty((cfg.batch, cfg.heads_q), dtype=torch.float32, device=qd.device)
     _check(_L.load().bdk_decode_partial(
         cache.handle(), C.byref(c), C.c_void_p(qd.data_ptr()),
         C.c_void_p(kd.data_ptr()) if kd is not None else None,
@@ -447,17 +484,22 @@ def decode_partial(cache: KVCache, cfg: AttentionConfig, q, k_new=None, v_new=No
     return o, lse
 
 
-def merge_partials(o_parts, lse_parts):
+def merge_partials(o_parts, lse_parts, out=None):
     """combine (attention.cpp:142-162) of normalized partials:
-    o_parts [n, rows..., d], lse_parts [n, rows...] (CUDA fp32)."""
+    o_parts [n, rows..., d], lse_parts [n, rows...] (CUDA fp32; the part
+    dimension may be strided, e.g. views into one all-gathered buffer)."""
     n = o_parts.shape[0]
     d = o_parts.shape[-1]
     rows = lse_parts[0].numel()
-    o_parts = o_parts.contiguous().float()
-    lse_parts = lse_parts.contiguous().float()
-    out = torch.empty(o_parts.shape[1:], dtype=torch.float32, device=o_parts.device)
+    if o_parts.dtype != torch.float32 or lse_parts.dtype != torch.float32:
+        raise ShapeError("merge_partials needs fp32 partials")
+    if not (o_parts[0].is_contiguous() and lse_parts[0].is_contiguous()):
+        o_parts, lse_parts = o_parts.contiguous(), lse_parts.contiguous()
+    if out is None:
+        out = torch.empty(o_parts.shape[1:], dtype=torch.float32, device=o_parts.device)
     _check(_L.load().bdk_merge_partials(C.c_void_p(o_parts.data_ptr()),
                                         C.c_void_p(lse_parts.data_ptr()), n, rows, d,
+                                        o_parts.stride(0), lse_parts.stride(0),
                                         C.c_void_p(out.data_ptr()), _stream_ptr()))
     return out
 

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/bitdecode_b200.h"
@@ -38,6 +39,10 @@ struct bdk_cache {
   void* h_stage = nullptr;
   void* d_stage = nullptr;
   size_t stage_bytes = 0;
+  // attention-kernel timing (bdk_profile_begin/end): one event pair per launch
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+  size_t events_used = 0;
 };
 
 namespace {
@@ -196,6 +201,17 @@ bdk_status run_decode(bdk_cache* c, const bdk_attn_config* cfg, const void* q, c
   a.precise = c->precise;
   a.sm_scale_log2 = (1.0f / std::sqrt(static_cast<float>(cfg->head_dim))) * bdk::kLog2e;
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  if (c->profiling) {
+    if (c->events_used == c->events.size()) {
+      cudaEvent_t e0, e1;
+      BDK_CUDA(cudaEventCreate(&e0), "cudaEventCreate");
+      BDK_CUDA(cudaEventCreate(&e1), "cudaEventCreate");
+      c->events.emplace_back(e0, e1);
+    }
+    a.ev_begin = c->events[c->events_used].first;
+    a.ev_end = c->events[c->events_used].second;
+    c->events_used++;
+  }
   BDK_CUDA(bdk::launch_decode(c->dev, a, stream), "decode launch");
   if (k_new != nullptr) {  // mirror of the cache-update phase
     for (int i = 0; i < cells; ++i) {
@@ -315,6 +331,10 @@ bdk_status bdk_cache_destroy(bdk_cache* c) {
   cudaFree(c->dev.res_len);
   cudaFree(c->part_o);
   cudaFree(c->part_ml);
+  for (auto& ev : c->events) {
+    cudaEventDestroy(ev.first);
+    cudaEventDestroy(ev.second);
+  }
   if (c->h_stage) cudaFreeHost(c->h_stage);
   cudaFree(c->d_stage);
   delete c;
@@ -437,11 +457,15 @@ bdk_status bdk_decode_partial(bdk_cache* c, const bdk_attn_config* cfg, const vo
 }
 
 bdk_status bdk_merge_partials(const float* o, const float* lse, uint32_t n_parts, uint32_t rows,
-                              uint32_t d, float* out, void* stream) {
+                              uint32_t d, uint64_t o_stride, uint64_t lse_stride, float* out,
+                              void* stream) {
   if (n_parts == 0) return fail(BDK_EMPTY_INPUT, "combine: no partial outputs");
   if (!o || !lse || !out) return fail(BDK_INVALID_ARGUMENT, "null tensor");
+  if (o_stride < (uint64_t)rows * d || lse_stride < rows)
+    return fail(BDK_SHAPE_ERROR, "merge_partials: part stride smaller than a part");
   BDK_CUDA(bdk::launch_merge_partials(o, lse, static_cast<int>(n_parts), static_cast<int>(rows),
-                                      static_cast<int>(d), out, as_stream(stream)),
+                                      static_cast<int>(d), o_stride, lse_stride, out,
+                                      as_stream(stream)),
            "merge launch");
   return BDK_OK;
 }
@@ -608,6 +632,31 @@ bdk_status bdk_corrupt_word(bdk_cache* c, uint32_t b, uint32_t h, uint32_t blk, 
                           word_offset(G, word),
                       &value, 2, cudaMemcpyHostToDevice),
            "H2D word");
+  return BDK_OK;
+}
+
+bdk_status bdk_profile_begin(bdk_cache* c) {
+  if (!c) return fail(BDK_INVALID_ARGUMENT, "null cache");
+  c->profiling = true;
+  c->events_used = 0;
+  return BDK_OK;
+}
+
+bdk_status bdk_profile_end(bdk_cache* c, float* total_ms, uint32_t* launches) {
+  if (!c || !total_ms || !launches) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  c->profiling = false;
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  float sum = 0.f;
+  for (size_t i = 0; i < c->events_used; ++i) {
+    BDK_CUDA(cudaEventSynchronize(c->events[i].second), "cudaEventSynchronize");
+    float ms = 0.f;
+    BDK_CUDA(cudaEventElapsedTime(&ms, c->events[i].first, c->events[i].second),
+             "cudaEventElapsedTime");
+    sum += ms;
+  }
+  *total_ms = sum;
+  *launches = static_cast<uint32_t>(c->events_used);
+  c->events_used = 0;
   return BDK_OK;
 }
 

@@ -641,17 +641,17 @@ __global__ void combine_kernel(DevCache c, DecodeArgs a, int n_parts, int d) {
 }
 
 __global__ void merge_partials_kernel(const float* o, const float* lse, int n_parts, int rows,
-                                      int d, float* out) {
+                                      int d, size_t o_stride, size_t lse_stride, float* out) {
   const int row = blockIdx.x;
   for (int ch = threadIdx.x; ch < d; ch += blockDim.x) {
     float ms = -INFINITY;
-    for (int p = 0; p < n_parts; ++p) ms = fmaxf(ms, lse[(size_t)p * rows + row]);
+    for (int p = 0; p < n_parts; ++p) ms = fmaxf(ms, lse[p * lse_stride + row]);
     float acc = 0.f, l = 0.f;
     for (int p = 0; p < n_parts; ++p) {
-      const float m = lse[(size_t)p * rows + row];
+      const float m = lse[p * lse_stride + row];
       if (m == -INFINITY) continue;
       const float w = ex2(m - ms);
-      acc += o[((size_t)p * rows + row) * d + ch] * w;
+      acc += o[p * o_stride + (size_t)row * d + ch] * w;
       l += w;
     }
     out[(size_t)row * d + ch] = l > 0.f ? acc / l : 0.f;
@@ -659,6 +659,33 @@ __global__ void merge_partials_kernel(const float* o, const float* lse, int n_pa
 }
 
 // ------------------------------------------------------------- launchers
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device,
+// size high-water mark) instead of on every launch (host-side latency of the
+// steady-state decode loop).
+static cudaError_t ensure_smem(const void* kern, size_t bytes) {
+  struct Entry {
+    const void* k;
+    int dev;
+    size_t bytes;
+  };
+  static Entry table[256];
+  static int n = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (int i = 0; i < n; ++i)
+    if (table[i].k == kern && table[i].dev == dev && table[i].bytes >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(std::max<size_t>(bytes, 16)));
+  if (e != cudaSuccess) return e;
+  for (int i = 0; i < n; ++i)
+    if (table[i].k == kern && table[i].dev == dev) {
+      table[i].bytes = bytes;
+      return cudaSuccess;
+    }
+  if (n < 256) table[n++] = Entry{kern, dev, bytes};
+  return cudaSuccess;
+}
 
 bool fast_path_ok(const Geom& G) {
   if (G.d != 128) return false;
@@ -677,13 +704,14 @@ static cudaError_t decode_launch(const DevCache& c, const DecodeArgs& a, cudaStr
   const size_t qp = (size_t)c.G.n_r * D;
   const size_t smem = std::max(ring, std::max(merge, qp));
   auto kern = decode_kernel<BITS, D, WN>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   dim3 grid(1 + a.n_splits, c.G.batch * c.G.heads_kv);
+  if (a.ev_begin) cudaEventRecord(a.ev_begin, s);
   kern<<<grid, C::NT, smem, s>>>(c, a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (a.ev_end) cudaEventRecord(a.ev_end, s);
   const int nthr = std::min(1024, std::max(32, a.n_group * D));
   combine_kernel<<<c.G.batch * c.G.heads_kv, nthr, 0, s>>>(c, a, 1 + a.n_splits, D);
   return cudaGetLastError();
@@ -771,8 +799,8 @@ cudaError_t launch_dequant(const DevCache& c, int cell, int blk0, int nblk, __ha
 }
 
 cudaError_t launch_merge_partials(const float* o, const float* lse, int n_parts, int rows, int d,
-                                  float* out, cudaStream_t s) {
-  merge_partials_kernel<<<rows, 128, 0, s>>>(o, lse, n_parts, rows, d, out);
+                                  size_t o_stride, size_t lse_stride, float* out, cudaStream_t s) {
+  merge_partials_kernel<<<rows, 128, 0, s>>>(o, lse, n_parts, rows, d, o_stride, lse_stride, out);
   return cudaGetLastError();
 }
 

@@ -32,6 +32,9 @@ struct DecodeArgs {
   int blk_begin = 0, blk_end = 1 << 30;  // packed block range attended
   int precise = 0;                        // hi/lo split P
   float sm_scale_log2 = 0.f;
+  // optional CUDA events recorded on the launching stream immediately before
+  // and after the attention kernel (bdk_profile_begin/end)
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
 };
 
 bool fast_path_ok(const Geom& G);
@@ -49,6 +52,6 @@ cudaError_t launch_dequant(const DevCache& c, int cell, int blk0, int nblk, __ha
 // merge normalized (o, lse) partials of n_parts ranks: o [n_parts][rows][d],
 // lse [n_parts][rows] (log2 domain) -> out [rows][d]
 cudaError_t launch_merge_partials(const float* o, const float* lse, int n_parts, int rows, int d,
-                                  float* out, cudaStream_t s);
+                                  size_t o_stride, size_t lse_stride, float* out, cudaStream_t s);
 
 }  // namespace bdk
