@@ -56,7 +56,10 @@ class SeqSplitComm:
         self.world, self.rows, self.d, self.group = world, rows, d, group
         self.part = rows * d + rows
         self.send = torch.zeros(self.part, dtype=torch.float32, device=device)
-        self.recv = torch.zeros((world, self.part), dtype=torch.float32, device=device)
+        # flat receive buffer (gloo's all_gather_into_tensor wants 1-D);
+        # recv2d is the [world, part] view
+        self.recv = torch.zeros(world * self.part, dtype=torch.float32, device=device)
+        self.recv2d = self.recv.view(world, self.part)
         self.o = self.send[: rows * d].view(rows, d)
         self.lse = self.send[rows * d:]
 
@@ -67,9 +70,9 @@ class SeqSplitComm:
         if self.world > 1:
             dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
         else:
-            self.recv[0].copy_(self.send)
-        o_parts = self.recv[:, : self.rows * self.d].unflatten(1, (self.rows, self.d))
-        lse_parts = self.recv[:, self.rows * self.d:]
+            self.recv2d[0].copy_(self.send)
+        o_parts = self.recv2d[:, : self.rows * self.d].unflatten(1, (self.rows, self.d))
+        lse_parts = self.recv2d[:, self.rows * self.d:]
         return o_parts, lse_parts
 
     def merge(self, out):
