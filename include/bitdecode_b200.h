@@ -139,16 +139,18 @@ BDK_API bdk_status bdk_decode_step_host(bdk_cache* cache, const bdk_attn_config*
                                         const float* q_host, const float* k_new_host,
                                         const float* v_new_host, float* out_host);
 /* Partial decode for sequence-split multi-GPU: attends packed blocks
- * [blk_begin, blk_end) of every cell plus the residual; appends only when
+ * [blk_begin, blk_end) of every cell plus (unless flags has
+ * BDK_PARTIAL_NO_RESIDUAL) the residual window; appends only when
  * k_new_dev != NULL.  Writes the NORMALIZED partial output out_dev
  * [batch][heads_q][d] and its log2-sum-exp lse_dev [batch][heads_q]; the
  * partials of all ranks merge with bdk_merge_partials (combine,
  * attention.cpp:142-162). */
+#define BDK_PARTIAL_NO_RESIDUAL 1u
 BDK_API bdk_status bdk_decode_partial(bdk_cache* cache, const bdk_attn_config* cfg,
                                       const void* q_dev, const void* k_new_dev,
                                       const void* v_new_dev, uint32_t blk_begin,
-                                      uint32_t blk_end, float* out_dev, float* lse_dev,
-                                      void* stream);
+                                      uint32_t blk_end, uint32_t flags, float* out_dev,
+                                      float* lse_dev, void* stream);
 /* LSE merge of n_parts normalized partials: part p is o_dev + p*o_stride
  * ([rows][d] fp32) and lse_dev + p*lse_stride ([rows], log2 domain), strides
  * in floats (so one all-gathered [n_parts][rows*d + rows] buffer merges in
@@ -193,6 +195,9 @@ BDK_API bdk_status bdk_corrupt_word(bdk_cache* cache, uint32_t b, uint32_t h, ui
  * bench.py's roofline; no reference counterpart). */
 BDK_API bdk_status bdk_profile_begin(bdk_cache* cache);
 BDK_API bdk_status bdk_profile_end(bdk_cache* cache, float* total_ms, uint32_t* launches);
+/* Total sm_100a kernels launched on behalf of this cache so far (every entry
+ * point; bench.py reports the delta over its timed region). */
+BDK_API bdk_status bdk_launch_count(const bdk_cache* cache, uint64_t* n);
 /* Blocks until all work on the cache's device is done; reports async errors. */
 BDK_API bdk_status bdk_synchronize(void);
 

@@ -50,8 +50,8 @@ SIGNATURES = {
     "bdk_flush_residual": (C.c_int, [vp, u32, u32, vp]),
     "bdk_decode_step": (C.c_int, [vp, C.POINTER(AttnConfig), vp, vp, vp, vp, vp]),
     "bdk_decode_step_host": (C.c_int, [vp, C.POINTER(AttnConfig), fp, fp, fp, fp]),
-    "bdk_decode_partial": (C.c_int, [vp, C.POINTER(AttnConfig), vp, vp, vp, u32, u32, vp, vp,
-                                     vp]),
+    "bdk_decode_partial": (C.c_int, [vp, C.POINTER(AttnConfig), vp, vp, vp, u32, u32, u32, vp,
+                                     vp, vp]),
     "bdk_merge_partials": (C.c_int, [vp, vp, u32, u32, u32, C.c_uint64, C.c_uint64, vp, vp]),
     "bdk_set_precise": (C.c_int, [vp, C.c_int]),
     "bdk_read_block": (C.c_int, [vp, u32, u32, u32, u16p, u16p, u16p, u16p]),
@@ -62,6 +62,7 @@ SIGNATURES = {
     "bdk_corrupt_word": (C.c_int, [vp, u32, u32, u32, u32, u16]),
     "bdk_profile_begin": (C.c_int, [vp]),
     "bdk_profile_end": (C.c_int, [vp, fp, C.POINTER(u32)]),
+    "bdk_launch_count": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
     "bdk_synchronize": (C.c_int, []),
 }
 

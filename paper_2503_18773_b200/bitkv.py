@@ -383,6 +383,12 @@ class KVCache:
         _check(_L.load().bdk_profile_end(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    def launch_count(self) -> int:
+        """sm_100a kernels launched for this cache so far (bdk_launch_count)."""
+        n = C.c_uint64()
+        _check(_L.load().bdk_launch_count(self._h, C.byref(n)))
+        return n.value
+
     def set_precise(self, precise: bool) -> None:
         """fp16 P (False) or P_hi + P_lo split PV (True), SURVEY.md F4."""
         _check(_L.load().bdk_set_precise(self._h, 1 if precise else 0))
@@ -461,9 +467,20 @@ class DecodeStepper:
         if st:
             _check(st)
 
+    def step(self, q, k_new, v_new, stream=None) -> None:
+        """Same call on other (contiguous CUDA fp16, same-shape) input
+        tensors, e.g. one preloaded slice per step; writes the bound out."""
+        a = self._args
+        st = self._fn(a[0], a[1], C.c_void_p(q.data_ptr()), C.c_void_p(k_new.data_ptr()),
+                      C.c_void_p(v_new.data_ptr()), a[5],
+                      stream if stream is not None else _stream_ptr())
+        if st:
+            _check(st)
+
 
 def decode_partial(cache: KVCache, cfg: AttentionConfig, q, k_new=None, v_new=None,
-                   blk_begin: int = 0, blk_end: int = 1 << 30, out=None, lse=None):
+                   blk_begin: int = 0, blk_end: int = 1 << 30, out=None, lse=None,
+                   include_residual: bool = True):
     """Sequence-split partial (see bdk_decode_partial): returns the normalized
     partial output [batch, heads_q, d] and its log2-sum-exp [batch, heads_q].
     k_new/v_new None: attend only (no append, no commit)."""
@@ -479,8 +496,8 @@ def decode_partial(cache: KVCache, cfg: AttentionConfig, q, k_new=None, v_new=No
         cache.handle(), C.byref(c), C.c_void_p(qd.data_ptr()),
         C.c_void_p(kd.data_ptr()) if kd is not None else None,
         C.c_void_p(vd.data_ptr()) if vd is not None else None, blk_begin,
-        min(blk_end, (1 << 32) - 1), C.c_void_p(o.data_ptr()), C.c_void_p(lse.data_ptr()),
-        _stream_ptr()))
+        min(blk_end, (1 << 32) - 1), 0 if include_residual else 1, C.c_void_p(o.data_ptr()),
+        C.c_void_p(lse.data_ptr()), _stream_ptr()))
     return o, lse
 
 

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -39,8 +40,16 @@ struct bdk_cache {
   void* h_stage = nullptr;
   void* d_stage = nullptr;
   size_t stage_bytes = 0;
+  // fast-path (stream-K) resources
+  int* unit_off = nullptr;            // device [cells + 1]
+  std::vector<int> unit_off_host;     // last uploaded schedule
+  int* counters = nullptr;            // device [cells]
+  float* slots = nullptr;             // device partial slots
+  size_t slot_floats = 0;
+  int fast_ctas_per_sm = -1, fast_ng = -1;
   // attention-kernel timing (bdk_profile_begin/end): one event pair per launch
   bool profiling = false;
+  mutable uint64_t launches = 0;  // kernels this cache has launched (all entry points)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
   size_t events_used = 0;
 };
@@ -162,10 +171,140 @@ bdk_status check_decode(bdk_cache* c, const bdk_attn_config* cfg, bool appends) 
   return BDK_OK;
 }
 
+bdk_status next_events(bdk_cache* c, cudaEvent_t* e0, cudaEvent_t* e1) {
+  *e0 = *e1 = nullptr;
+  if (!c->profiling) return BDK_OK;
+  if (c->events_used == c->events.size()) {
+    cudaEvent_t a, b;
+    BDK_CUDA(cudaEventCreate(&a), "cudaEventCreate");
+    BDK_CUDA(cudaEventCreate(&b), "cudaEventCreate");
+    c->events.emplace_back(a, b);
+  }
+  *e0 = c->events[c->events_used].first;
+  *e1 = c->events[c->events_used].second;
+  c->events_used++;
+  return BDK_OK;
+}
+
+// Stream-K fast path (bdk_decode_fast.cu): schedule from the host mirror of
+// the lengths, one launch for append + attention + combine, then the flush of
+// any residual the step filled.
+bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void* q,
+                           const void* k_new, const void* v_new, float* out, float* lse,
+                           int blk_begin, int blk_end, cudaStream_t stream, bool no_res) {
+  const int cells = static_cast<int>(c->desc.batch * c->desc.heads_kv);
+  const int ng = static_cast<int>(cfg->heads_q / cfg->heads_kv);
+  const Geom& G = c->dev.G;
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  if (c->fast_ng != ng) {
+    c->fast_ctas_per_sm = bdk::fast_decode_ctas_per_sm(G, ng);
+    c->fast_ng = ng;
+    if (c->fast_ctas_per_sm <= 0)
+      return fail(BDK_CUDA_ERROR, "fast decode kernel does not fit on this device");
+  }
+  // schedule: [unit_off (cells + 1) | unit_nb (cells)]; a cell's units are its
+  // packed blocks in range then ceil(res_len' / (16 * warp_n)) residual units
+  const int rt = bdk::fast_residual_tokens(G);
+  std::vector<int> off(2 * cells + 1, 0);
+  for (int i = 0; i < cells; ++i) {
+    const int nb = std::max(0, std::min(blk_end, c->packed_blocks[i]) - blk_begin);
+    const int rlen = no_res ? 0 : c->res_len[i] + (k_new != nullptr ? 1 : 0);
+    const int nres = std::max(1, (rlen + rt - 1) / rt);
+    off[i + 1] = off[i] + nb + nres;
+    off[cells + 1 + i] = nb;
+  }
+  if (!c->unit_off) {
+    BDK_CUDA(cudaMalloc(&c->unit_off, (2 * cells + 1) * sizeof(int)), "cudaMalloc(schedule)");
+    BDK_CUDA(cudaMalloc(&c->counters, cells * sizeof(int)), "cudaMalloc(counters)");
+    BDK_CUDA(cudaMemset(c->counters, 0, cells * sizeof(int)), "cudaMemset(counters)");
+  }
+  if (off != c->unit_off_host) {
+    BDK_CUDA(cudaMemcpyAsync(c->unit_off, off.data(), (2 * cells + 1) * sizeof(int),
+                             cudaMemcpyHostToDevice, stream),
+             "H2D schedule");
+    c->unit_off_host = off;
+  }
+  const long long T = off[cells];
+  const int n_ctas =
+      static_cast<int>(std::min<long long>(T, (long long)c->fast_ctas_per_sm * c->num_sms));
+  const size_t need = (size_t)(n_ctas + cells) * bdk::slot_stride(ng);
+  if (need > c->slot_floats) {
+    if (c->slots) cudaFree(c->slots);
+    c->slots = nullptr;
+    BDK_CUDA(cudaMalloc(&c->slots, need * sizeof(float)), "cudaMalloc(slots)");
+    c->slot_floats = need;
+  }
+  bdk::FastArgs a;
+  a.q = static_cast<const __half*>(q);
+  a.k_new = static_cast<const __half*>(k_new);
+  a.v_new = static_cast<const __half*>(v_new);
+  a.out = out;
+  a.out_lse = lse;
+  a.slots = c->slots;
+  a.counters = c->counters;
+  a.unit_off = c->unit_off;
+  a.unit_nb = c->unit_off + cells + 1;
+  a.total_units = T;
+  a.n_ctas = n_ctas;
+  a.heads_q = static_cast<int>(cfg->heads_q);
+  a.n_group = ng;
+  a.blk_begin = blk_begin;
+  a.skip_residual = no_res ? 1 : 0;
+  a.sm_scale_log2 = (1.0f / std::sqrt(static_cast<float>(cfg->head_dim))) * bdk::kLog2e;
+  bdk_status st = next_events(c, &a.ev_begin, &a.ev_end);
+  if (st) return st;
+  // dev knob: BDK_TRACE=<file> appends per-CTA globaltimer stamps of every
+  // fast launch (synchronizes; never set in measurements)
+  static const char* trace_path = getenv("BDK_TRACE");
+  static const int dev_flags = getenv("BDK_DEV_FLAGS") ? atoi(getenv("BDK_DEV_FLAGS")) : 0;
+  a.dev_flags = dev_flags;
+  unsigned long long* trace = nullptr;
+  if (trace_path) {
+    BDK_CUDA(cudaMalloc(&trace, (size_t)n_ctas * 16 * 8), "cudaMalloc(trace)");
+    BDK_CUDA(cudaMemsetAsync(trace, 0, (size_t)n_ctas * 16 * 8, stream), "memset(trace)");
+    a.trace = trace;
+  }
+  BDK_CUDA(bdk::launch_decode_fast(c->dev, a, stream), "fast decode launch");
+  c->launches += 1;
+  if (trace) {
+    std::vector<unsigned long long> h((size_t)n_ctas * 16);
+    BDK_CUDA(cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, stream),
+             "D2H trace");
+    BDK_CUDA(cudaStreamSynchronize(stream), "trace sync");
+    cudaFree(trace);
+    if (FILE* f = fopen(trace_path, "a")) {
+      fprintf(f, "launch n_ctas=%d T=%lld\n", n_ctas, T);
+      for (int i = 0; i < n_ctas; ++i) {
+        for (int k = 0; k < 16; ++k) fprintf(f, "%llu ", h[(size_t)i * 16 + k]);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+  }
+  if (k_new != nullptr) {
+    bool any_full = false;
+    for (int i = 0; i < cells; ++i) any_full |= (c->res_len[i] + 1 == G.n_r);
+    if (any_full) {
+      BDK_CUDA(bdk::launch_flush_full(c->dev, stream), "flush launch");
+      c->launches += 1;
+    }
+    for (int i = 0; i < cells; ++i) {
+      if (++c->res_len[i] == G.n_r) {
+        c->res_len[i] = 0;
+        c->packed_blocks[i] += 1;
+      }
+    }
+  }
+  return BDK_OK;
+}
+
 bdk_status run_decode(bdk_cache* c, const bdk_attn_config* cfg, const void* q, const void* k_new,
                       const void* v_new, float* out, float* lse, int blk_begin, int blk_end,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, bool no_res = false) {
   const int cells = static_cast<int>(c->desc.batch * c->desc.heads_kv);
+  if (!c->precise && bdk::fast_decode_ok(c->dev.G, static_cast<int>(cfg->heads_q / cfg->heads_kv)))
+    return run_decode_fast(c, cfg, q, k_new, v_new, out, lse, std::max(0, blk_begin), blk_end,
+                           stream, no_res);
   int nblk_max = 0;
   for (int i = 0; i < cells; ++i) nblk_max = std::max(nblk_max, c->packed_blocks[i]);
   const int lo = std::max(0, blk_begin), hi = std::min(blk_end, nblk_max);
@@ -198,21 +337,16 @@ bdk_status run_decode(bdk_cache* c, const bdk_attn_config* cfg, const void* q, c
   a.blocks_per_split = bps;
   a.blk_begin = lo;
   a.blk_end = hi;
+  a.skip_residual = no_res ? 1 : 0;
   a.precise = c->precise;
   a.sm_scale_log2 = (1.0f / std::sqrt(static_cast<float>(cfg->head_dim))) * bdk::kLog2e;
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
-  if (c->profiling) {
-    if (c->events_used == c->events.size()) {
-      cudaEvent_t e0, e1;
-      BDK_CUDA(cudaEventCreate(&e0), "cudaEventCreate");
-      BDK_CUDA(cudaEventCreate(&e1), "cudaEventCreate");
-      c->events.emplace_back(e0, e1);
-    }
-    a.ev_begin = c->events[c->events_used].first;
-    a.ev_end = c->events[c->events_used].second;
-    c->events_used++;
+  {
+    bdk_status st = next_events(c, &a.ev_begin, &a.ev_end);
+    if (st) return st;
   }
   BDK_CUDA(bdk::launch_decode(c->dev, a, stream), "decode launch");
+  c->launches += 2;  // split-KV kernel + combine kernel
   if (k_new != nullptr) {  // mirror of the cache-update phase
     for (int i = 0; i < cells; ++i) {
       if (++c->res_len[i] == c->dev.G.n_r) {
@@ -331,6 +465,9 @@ bdk_status bdk_cache_destroy(bdk_cache* c) {
   cudaFree(c->dev.res_len);
   cudaFree(c->part_o);
   cudaFree(c->part_ml);
+  cudaFree(c->unit_off);
+  cudaFree(c->counters);
+  cudaFree(c->slots);
   for (auto& ev : c->events) {
     cudaEventDestroy(ev.first);
     cudaEventDestroy(ev.second);
@@ -375,6 +512,7 @@ bdk_status bdk_prefill(bdk_cache* c, uint32_t b, uint32_t h, const void* k, cons
   if (nb > c->dev.G.max_blocks) return fail(BDK_CAPACITY_ERROR, "prefill exceeds max_tokens");
   if (len > 0 && (!k || !v)) return fail(BDK_INVALID_ARGUMENT, "null k/v");
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  c->launches += 1;
   BDK_CUDA(bdk::launch_prefill(c->dev, static_cast<const __half*>(k),
                                static_cast<const __half*>(v), static_cast<int>(len), i, 1,
                                as_stream(stream)),
@@ -394,6 +532,7 @@ bdk_status bdk_prefill_all(bdk_cache* c, const void* k, const void* v, uint32_t 
   if (nb > c->dev.G.max_blocks) return fail(BDK_CAPACITY_ERROR, "prefill exceeds max_tokens");
   const int cells = static_cast<int>(c->res_len.size());
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  c->launches += 1;
   BDK_CUDA(bdk::launch_prefill(c->dev, static_cast<const __half*>(k),
                                static_cast<const __half*>(v), static_cast<int>(len), 0, cells,
                                as_stream(stream)),
@@ -413,6 +552,7 @@ bdk_status bdk_append_token(bdk_cache* c, uint32_t b, uint32_t h, const void* k,
   if (c->res_len[i] == c->dev.G.n_r)
     return fail(BDK_CAPACITY_ERROR, "residual is full; flush before appending");
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  c->launches += 1;
   BDK_CUDA(bdk::launch_append(c->dev, i, static_cast<const __half*>(k),
                               static_cast<const __half*>(v), as_stream(stream)),
            "append launch");
@@ -430,6 +570,7 @@ bdk_status bdk_flush_residual(bdk_cache* c, uint32_t b, uint32_t h, void* stream
   if (c->packed_blocks[i] >= c->dev.G.max_blocks)
     return fail(BDK_CAPACITY_ERROR, "cache arena full (raise max_tokens)");
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  c->launches += 1;
   BDK_CUDA(bdk::launch_flush(c->dev, i, as_stream(stream)), "flush launch");
   c->packed_blocks[i] += 1;
   c->res_len[i] = 0;
@@ -446,14 +587,19 @@ bdk_status bdk_decode_step(bdk_cache* c, const bdk_attn_config* cfg, const void*
 
 bdk_status bdk_decode_partial(bdk_cache* c, const bdk_attn_config* cfg, const void* q,
                               const void* k_new, const void* v_new, uint32_t blk_begin,
-                              uint32_t blk_end, float* out, float* lse, void* stream) {
+                              uint32_t blk_end, uint32_t flags, float* out, float* lse,
+                              void* stream) {
   const bool appends = k_new != nullptr;
   bdk_status s = check_decode(c, cfg, appends);
   if (s) return s;
   if (!q || !out || !lse || (appends && !v_new))
     return fail(BDK_INVALID_ARGUMENT, "null tensor");
+  const bool no_res = (flags & BDK_PARTIAL_NO_RESIDUAL) != 0;
+  if (no_res && appends)
+    return fail(BDK_STATE_ERROR, "decode_partial: an append needs the residual window");
   return run_decode(c, cfg, q, k_new, v_new, out, lse, static_cast<int>(blk_begin),
-                    static_cast<int>(std::min<uint32_t>(blk_end, 1u << 30)), as_stream(stream));
+                    static_cast<int>(std::min<uint32_t>(blk_end, 1u << 30)), as_stream(stream),
+                    no_res);
 }
 
 bdk_status bdk_merge_partials(const float* o, const float* lse, uint32_t n_parts, uint32_t rows,
@@ -599,6 +745,7 @@ bdk_status bdk_dequant_blocks(const bdk_cache* c, uint32_t b, uint32_t h, uint32
   if (static_cast<int>(blk0 + nblk) > c->packed_blocks[i])
     return fail(BDK_SHAPE_ERROR, "packed_tile: range past packed segment");
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  c->launches += 1;
   BDK_CUDA(bdk::launch_dequant(c->dev, i, static_cast<int>(blk0), static_cast<int>(nblk),
                                static_cast<__half*>(k_out), static_cast<__half*>(v_out),
                                as_stream(stream)),
@@ -657,6 +804,12 @@ bdk_status bdk_profile_end(bdk_cache* c, float* total_ms, uint32_t* launches) {
   *total_ms = sum;
   *launches = static_cast<uint32_t>(c->events_used);
   c->events_used = 0;
+  return BDK_OK;
+}
+
+bdk_status bdk_launch_count(const bdk_cache* c, uint64_t* n) {
+  if (!c || !n) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  *n = c->launches;
   return BDK_OK;
 }
 

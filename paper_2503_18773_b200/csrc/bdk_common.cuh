@@ -51,6 +51,18 @@ __host__ __device__ inline int pos_token(int p, int pack, int interleave) {
   return k < half ? pack - 1 - 2 * k : pack - 2 - 2 * (k - half);
 }
 
+// inverse of pos_token: bit-field position (from the LSB) holding token
+// offset j of a word
+__host__ __device__ inline int field_of_token(int j, int pack, int interleave) {
+  if (pack == 1) return 0;
+  int k;  // field index from the MSB
+  if (!interleave)
+    k = j;
+  else
+    k = (j & 1) ? (pack - 1 - j) / 2 : pack / 2 + (pack - 2 - j) / 2;
+  return pack - 1 - k;
+}
+
 // ------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -144,6 +156,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// wait with a suspend-time hint: producer-side waits that are expected to
+// block (ring full) park the warp instead of spinning on issue slots
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 // 1-D bulk copy global -> shared (TMA engine, SASS UBLKCP), completes on bar.
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                              uint64_t* bar, uint64_t policy) {
@@ -158,6 +190,12 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
   return p;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 // -------------------------------------------------------- warp reductions

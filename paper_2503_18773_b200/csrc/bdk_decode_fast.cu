@@ -1,0 +1,865 @@
+// bdk_decode_fast.cu -- the sm_100a decode hot kernel (fast mode).
+//
+// One launch performs decode_step's attention for every cell (attention.cpp:
+// 164-242): residual_attend + packed_attend + combine, with the append of the
+// new token fused in.  (The flush of a residual that became full runs as a
+// separate tiny launch, only on the steps where one fills.)
+//
+// Schedule -- stream-K over units.  Cell c (= b * heads_kv + h) owns
+// nb_c + 1 units: its packed blocks (in the attended range) and, last, its
+// residual window.  The grid is exactly the resident CTA capacity of the GPU;
+// CTA i takes units [i*T/N, (i+1)*T/N) of the flattened sequence, so every
+// SM streams the same number of blocks whatever the batch / context shape
+// (b=1 128K and b=32 8K alike).  A CTA range may span several cells; each
+// (CTA, cell) segment leaves one partial (unnormalized O, running max, sum)
+// in slot i + c (injective), and the CTA that completes a cell (atomic
+// counter) LSE-merges its partials into the output (combine,
+// attention.cpp:142-162).
+//
+// CTA = WN consumer warps + 1 TMA warp + 1 prep warp:
+//   TMA warp   one lane streams whole block records (K words | V words |
+//              K params | V params, ~17 KB) HBM -> SMEM with cp.async.bulk
+//              into an NS-stage mbarrier ring (full / empty barriers).
+//   prep warp  per block: folds the channel-wise K scales into the query,
+//              Q'[h][c] = fp16(q[h][c] * s_c), and the zero-points into one
+//              scalar per head, Z[h] = sum_c q[h][c] z_c (fp32); converts the
+//              per-token V (scale, zero) to fp32.  Signals a prep barrier.
+//   consumers  warp w owns 16-byte chunk w (8*P tokens) of every channel row:
+//              ldmatrix.trans (K) / ldmatrix (V) of the packed words, exact
+//              code extraction (lop3 + hsub2/hfma2, bdk_frag.cuh), mma.sync
+//              m16n8k16 in swap-AB form  S^T = codes_K . Q'^T  (tokens in M,
+//              GQA heads in N), online softmax in the exp2 domain with the
+//              logits S = S' + Z, then O^T += codes_V^T . (P s_t)^T  plus the
+//              per-head zero term sum_t P z_t accumulated in fp32.
+//
+// Numerics (fast mode): the folds replace the
+// reference's round_f16(code*scale + zero) staging by fp16(q*s) and fp16(P*s)
+// roundings of the same magnitude; the fp32 accumulation is unchanged.  The
+// bit-faithful dequant path is the exact kernel in bdk_kernels.cu.
+#include <cfloat>
+#include <cstdlib>
+
+#include "bdk_frag.cuh"
+#include "bdk_launch.h"
+
+namespace bdk {
+
+namespace {
+
+constexpr int D = 128;
+constexpr int KT = D / 16;
+constexpr int QP_ROW = 272;                    // bytes per Q' head row (256 + 16 pad)
+constexpr int QP_BYTES = 8 * QP_ROW + 8 * 4;  // Q' [8 heads] + Z [8] per K group
+constexpr int OT = KT;                        // O^T accumulator tiles
+constexpr int MERGE_KC = 16;                   // contributors per merge round
+
+template <int BITS, int WN, int MINB_, int GRP_>
+struct FC {
+  static constexpr int P = 16 / BITS;
+  static constexpr int NPAIR = P / 2;          // S^T m16 tiles per chunk (P >= 2)
+  static constexpr int RB = 16 * WN;           // bytes per channel row
+  static constexpr int GRP = GRP_;             // consumer groups (alternate blocks)
+  static constexpr int NC = WN * GRP;          // consumer warps
+  static constexpr int NT = (NC + 1 + GRP) * 32;  // + TMA warp + one prep warp per group
+  static constexpr int MINB = MINB_;
+};
+
+struct Smem {
+  uint32_t ring, prep, merge;  // byte offsets
+  uint32_t prep_stride;
+  uint32_t merge_floats;
+  uint32_t total;
+};
+
+__host__ __device__ inline Smem smem_layout(const Geom& G, int ng, int NS, int grp) {
+  Smem L;
+  const int gpb = G.k_axis == 0 ? G.n_r / G.g : 1;
+  L.ring = 0;
+  L.prep_stride = (uint32_t)(((gpb * QP_BYTES + G.n_r * 8) + 127) / 128 * 128);
+  L.prep = L.ring + NS * G.rec_bytes;
+  L.merge = L.prep + NS * L.prep_stride;
+  const uint32_t merge_bytes =
+      (uint32_t)(max(G.warp_n * grp * (ng * D + 16), 24 + 2 * MERGE_KC * 8) * 4 + 64);
+  L.merge_floats = merge_bytes / 4;
+  L.total = L.merge + merge_bytes + 3 * NS * 8 + 16;
+  return L;
+}
+
+__device__ __forceinline__ int cta_of_unit(long long u, long long T, int N) {
+  return (int)(((u + 1) * (long long)N - 1) / T);
+}
+
+__device__ __forceinline__ int find_cell(const int* off, int cells, long long u) {
+  int lo = 0, hi = cells - 1;  // largest c with off[c] <= u
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((long long)__ldg(off + mid) <= u)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// online-softmax state of one consumer warp (columns = heads 2*t4, 2*t4+1)
+struct Soft {
+  float m0, m1, l0, l1, z0, z1;  // z: sum_t P_t * zero_t (V zero-point term)
+};
+
+template <int KTILES>
+__device__ __forceinline__ void rescale(Soft& st, float (&o)[KTILES][4], float r0, float r1) {
+#pragma unroll
+  for (int mt = 0; mt < KTILES; ++mt) {
+    o[mt][0] *= r0;
+    o[mt][1] *= r1;
+    o[mt][2] *= r0;
+    o[mt][3] *= r1;
+  }
+  st.l0 *= r0;
+  st.l1 *= r1;
+  st.z0 *= r0;
+  st.z1 *= r1;
+}
+
+// Online softmax over NPAIR S^T tiles of logits x (log2 domain), in place:
+// x <- exp2(x - m).  Lazy rescaling: the running max m (warp-uniform per
+// head) is only raised -- with the cross-lane reduction and the O rescale --
+// when some logit exceeds it by more than TAU, so P <= 2^TAU and the common
+// path costs one vote instead of three shuffle rounds.  Exact in real
+// arithmetic; m only sets the scale of the fp32 state.
+constexpr float TAU = 6.f;
+
+template <int NPAIR>
+__device__ __forceinline__ void softmax_update(float (&x)[NPAIR][4], Soft& st, float (&o)[OT][4]) {
+  float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NPAIR; ++i) {
+    mx0 = fmaxf(mx0, fmaxf(x[i][0], x[i][2]));
+    mx1 = fmaxf(mx1, fmaxf(x[i][1], x[i][3]));
+  }
+  if (__any_sync(0xffffffffu, mx0 > st.m0 + TAU || mx1 > st.m1 + TAU)) {
+#pragma unroll
+    for (int off = 4; off <= 16; off <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+    }
+    const float mn0 = fmaxf(st.m0, mx0), mn1 = fmaxf(st.m1, mx1);
+    const float r0 = st.m0 == -INFINITY ? 0.f : ex2(st.m0 - mn0);
+    const float r1 = st.m1 == -INFINITY ? 0.f : ex2(st.m1 - mn1);
+    rescale<OT>(st, o, r0, r1);
+    st.m0 = mn0;
+    st.m1 = mn1;
+  }
+  const float b0 = st.m0 == -INFINITY ? 0.f : st.m0;
+  const float b1 = st.m1 == -INFINITY ? 0.f : st.m1;
+#pragma unroll
+  for (int i = 0; i < NPAIR; ++i) {
+    x[i][0] = ex2(x[i][0] - b0);
+    x[i][1] = ex2(x[i][1] - b1);
+    x[i][2] = ex2(x[i][2] - b0);
+    x[i][3] = ex2(x[i][3] - b1);
+    st.l0 += x[i][0] + x[i][2];
+    st.l1 += x[i][1] + x[i][3];
+  }
+}
+
+// consumer-warp partial of a segment -> CTA partial in `slot`
+template <int NC>
+__device__ __forceinline__ void finalize_segment(Soft st, float (&o)[OT][4], float* sm, int ng,
+                                                 float* slot, float oscale) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, t4 = lane & 3;
+#pragma unroll
+  for (int off = 4; off <= 16; off <<= 1) {
+    st.l0 += __shfl_xor_sync(0xffffffffu, st.l0, off);
+    st.l1 += __shfl_xor_sync(0xffffffffu, st.l1, off);
+    st.z0 += __shfl_xor_sync(0xffffffffu, st.z0, off);
+    st.z1 += __shfl_xor_sync(0xffffffffu, st.z1, off);
+  }
+  const int WS = ng * D + 16;
+  float* so = sm + warp * WS;
+  const int h0 = 2 * t4, h1 = 2 * t4 + 1;
+#pragma unroll
+  for (int mt = 0; mt < KT; ++mt) {
+    const int ch = mt * 16 + gid;
+    // undo the subnormal-mode scale of the V codes (2^(24 - SH_REF)) and add
+    // the zero-point term
+    if (h0 < ng) {
+      so[h0 * D + ch] = fmaf(o[mt][0], oscale, st.z0);
+      so[h0 * D + ch + 8] = fmaf(o[mt][2], oscale, st.z0);
+    }
+    if (h1 < ng) {
+      so[h1 * D + ch] = fmaf(o[mt][1], oscale, st.z1);
+      so[h1 * D + ch + 8] = fmaf(o[mt][3], oscale, st.z1);
+    }
+  }
+  if (gid == 0) {
+    if (h0 < ng) {
+      so[ng * D + h0] = st.m0;
+      so[ng * D + 8 + h0] = st.l0;
+    }
+    if (h1 < ng) {
+      so[ng * D + h1] = st.m1;
+      so[ng * D + 8 + h1] = st.l1;
+    }
+  }
+  named_bar(1, NC * 32);
+  for (int i = threadIdx.x; i < ng * D; i += NC * 32) {
+    const int h = i / D;
+    float ms = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < NC; ++w) ms = fmaxf(ms, sm[w * WS + ng * D + h]);
+    float acc = 0.f, l = 0.f;
+#pragma unroll
+    for (int w = 0; w < NC; ++w) {
+      const float mw = sm[w * WS + ng * D + h];
+      const float f = mw == -INFINITY ? 0.f : ex2(mw - ms);
+      acc += sm[w * WS + i] * f;
+      l += sm[w * WS + ng * D + 8 + h] * f;
+    }
+    slot[i] = acc;
+    if ((i % D) == 0) {
+      slot[ng * D + 2 * h] = ms;
+      slot[ng * D + 2 * h + 1] = l;
+    }
+  }
+  named_bar(1, NC * 32);
+}
+
+// LSE merge of all partials of `cell` (combine, attention.cpp:142-162).
+// It runs on the kernel's tail, so it is written for latency: per chunk of
+// up to 32 contributors, (1) all (max, sum) pairs are fetched in one round
+// into shared memory and turned into per-head weights there, (2) every thread
+// owns float4s of the output and issues the chunk's loads back to back.
+template <int NC>
+__device__ void merge_cell(const FastArgs& a, const Geom& G, int cell, int cta_lo, int cta_hi,
+                           float* sm) {
+  constexpr int NTH = NC * 32;
+  constexpr int NV = (8 * D / 4 + NTH - 1) / NTH;  // float4 outputs per thread (max)
+  const int ng = a.n_group;
+  const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
+  const int stride = slot_stride(ng);
+  const float* base = a.slots + (size_t)(cta_lo + cell) * stride;
+  const int nk = cta_hi - cta_lo + 1;
+  float* msh = sm;        // [8] running max per head
+  float* lsh = sm + 8;    // [8] running sum per head
+  float* rsh = sm + 16;   // [8] rescale of the previous chunks
+  float* wk = sm + 24;    // [MERGE_KC][8] weights
+  float* lk = wk + MERGE_KC * 8;  // [MERGE_KC][8] sums
+  const int nvec = ng * D / 4;
+  float4 acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x < 8) {
+    msh[threadIdx.x] = -INFINITY;
+    lsh[threadIdx.x] = 0.f;
+  }
+  for (int k0 = 0; k0 < nk; k0 += MERGE_KC) {
+    const int kc = min(MERGE_KC, nk - k0);
+    for (int idx = threadIdx.x; idx < kc * ng; idx += NTH) {
+      const int k = idx / ng, h = idx % ng;
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(
+          base + (size_t)(k0 + k) * stride + ng * D + 2 * h));
+      wk[k * 8 + h] = ml.x;
+      lk[k * 8 + h] = ml.y;
+    }
+    named_bar(1, NTH);
+    if (threadIdx.x < ng) {
+      const int h = threadIdx.x;
+      const float mo = msh[h];
+      float mx = mo;
+      for (int k = 0; k < kc; ++k) mx = fmaxf(mx, wk[k * 8 + h]);
+      const float r = mo == -INFINITY ? 0.f : ex2(mo - mx);
+      float l = lsh[h] * r;
+      for (int k = 0; k < kc; ++k) {
+        const float m = wk[k * 8 + h];
+        const float w = m == -INFINITY ? 0.f : ex2(m - mx);
+        wk[k * 8 + h] = w;
+        l = fmaf(lk[k * 8 + h], w, l);
+      }
+      lsh[h] = l;
+      msh[h] = mx;
+      rsh[h] = r;
+    }
+    named_bar(1, NTH);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int e = threadIdx.x + v * NTH;
+      if (e < nvec) {
+        const int h = (4 * e) / D;
+        const float r = rsh[h];
+        float4 s4 = make_float4(acc[v].x * r, acc[v].y * r, acc[v].z * r, acc[v].w * r);
+        const float4* po = reinterpret_cast<const float4*>(base + (size_t)k0 * stride) + e;
+        const int st4 = stride / 4;
+        float4 o[MERGE_KC];
+#pragma unroll
+        for (int k = 0; k < MERGE_KC; ++k)
+          o[k] = k < kc ? __ldcg(po + (size_t)k * st4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < MERGE_KC; ++k) {
+          const float w = k < kc ? wk[k * 8 + h] : 0.f;
+          s4.x = fmaf(o[k].x, w, s4.x);
+          s4.y = fmaf(o[k].y, w, s4.y);
+          s4.z = fmaf(o[k].z, w, s4.z);
+          s4.w = fmaf(o[k].w, w, s4.w);
+        }
+        acc[v] = s4;
+      }
+    }
+    named_bar(1, NTH);  // wk / lk reused by the next chunk
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int e = threadIdx.x + v * NTH;
+    if (e < nvec) {
+      const int h = (4 * e) / D, ch = (4 * e) % D;
+      const float l = lsh[h];
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const size_t row = (size_t)bidx * a.heads_q + (size_t)hk * ng + h;
+      const float4 s4 = acc[v];
+      *reinterpret_cast<float4*>(a.out + row * D + ch) =
+          make_float4(s4.x * inv, s4.y * inv, s4.z * inv, s4.w * inv);
+      if (a.out_lse != nullptr && ch == 0)
+        a.out_lse[row] = l > 0.f ? msh[h] + __log2f(l) : -INFINITY;
+    }
+  }
+}
+
+template <int BITS, int WN, int NS, int MINB, int GRP>
+__global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
+    decode_fast_kernel(DevCache c, FastArgs a) {
+  using C = FC<BITS, WN, MINB, GRP>;
+  constexpr int P = C::P, NPAIR = C::NPAIR, NC = C::NC, RB = C::RB;
+  static_assert(NS % GRP == 0, "stage s must always belong to consumer group s % GRP");
+  // subnormal mode: the V operand P s is pre-scaled by 2^(SH_REF - sh) so the
+  // accumulator holds O * 2^(SH_REF - 24) for every field shift sh
+  constexpr int SH_REF = BITS == 8 ? 0 : 2;
+  const float oscale = exp2f((float)(24 - SH_REF));
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const Geom& G = c.G;
+  const int cells = G.batch * G.heads_kv;
+  const int ng = a.n_group;
+  const Smem L = smem_layout(G, ng, NS, GRP);
+  uint8_t* ring = smem + L.ring;
+  uint8_t* prep = smem + L.prep;
+  float* merge_sm = reinterpret_cast<float*>(smem + L.merge);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.total - 3 * NS * 8 - 16);
+  uint64_t* empty = full + NS;
+  uint64_t* ready = empty + NS;
+  int* flag = reinterpret_cast<int*>(ready + NS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, t4 = lane & 3;
+  const int REC = G.rec_bytes;
+
+  // zero the prep areas once: Q' rows of heads >= n_group stay zero
+  for (uint32_t i = threadIdx.x * 16; i < NS * L.prep_stride; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(prep + i) = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], WN);  // the WN warps of the group that owns stage s
+      mbar_init(&ready[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const long long T = a.total_units;
+  const int N = a.n_ctas;
+  const long long u_begin = (long long)blockIdx.x * T / N;
+  const long long u_end = (long long)(blockIdx.x + 1) * T / N;
+  if (u_begin >= u_end) return;
+  const int cell0 = find_cell(a.unit_off, cells, u_begin);
+  unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * 16 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer();
+
+  // ------------------------------------------------------------ TMA warp
+  if (warp == NC) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int it = 0;
+      long long u = u_begin;
+      for (int cell = cell0; u < u_end; ++cell) {
+        const long long cb = __ldg(a.unit_off + cell), ce = __ldg(a.unit_off + cell + 1);
+        const long long seg_end = min(u_end, ce);
+        const long long pk_end = min(seg_end, cb + (long long)__ldg(a.unit_nb + cell));
+        const uint8_t* base = c.records + (size_t)cell * G.max_blocks * REC;
+        for (long long x = u; x < pk_end; ++x, ++it) {
+          const int s = it % NS;
+          if (it >= NS) mbar_wait_sleep(&empty[s], ((it / NS) - 1) & 1);
+          mbar_expect_tx(&full[s], (uint32_t)REC);
+          const int blk = a.blk_begin + (int)(x - cb);
+          tma_bulk_g2s(ring + (size_t)s * REC, base + (size_t)blk * REC, (uint32_t)REC, &full[s],
+                       pol);
+        }
+        u = seg_end;
+      }
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------- prep warps
+  if (warp > NC) {
+    const int pgrp = warp - NC - 1;  // prepares the blocks of consumer group pgrp
+    const int gpb = G.k_axis == 0 ? G.n_r / G.g : 1;
+    const int h = lane & 7, cbk = lane >> 3;  // head, 32-channel block
+
+    int it = 0;
+    long long u = u_begin;
+    for (int cell = cell0; u < u_end; ++cell) {
+      const long long ce = __ldg(a.unit_off + cell + 1);
+      const long long seg_end = min(u_end, ce);
+      const long long pk_end =
+          min(seg_end, (long long)__ldg(a.unit_off + cell) + __ldg(a.unit_nb + cell));
+      if (u < pk_end) {
+        const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
+        // lanes of heads >= n_group carry q = 0: they write the zero Q' rows
+        uint32_t q2[16];
+        float qf[32];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) q2[i] = 0u;
+        if (h < ng) {
+          const uint4* qs = reinterpret_cast<const uint4*>(
+              a.q + ((size_t)bidx * a.heads_q + (size_t)hk * ng + h) * D + cbk * 32);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const uint4 w = __ldg(qs + v);
+            q2[4 * v] = w.x;
+            q2[4 * v + 1] = w.y;
+            q2[4 * v + 2] = w.z;
+            q2[4 * v + 3] = w.w;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 f = __half22float2(u2h(q2[i]));
+          qf[2 * i] = f.x;
+          qf[2 * i + 1] = f.y;
+        }
+        for (long long x = u; x < pk_end; ++x, ++it) {
+          if (GRP > 1 && (it % GRP) != pgrp) continue;
+          const int s = it % NS;
+          mbar_wait_sleep(&full[s], (it / NS) & 1);
+          if (a.dev_flags & 2) {  // dev probe: no prep work
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ready[s]);
+            continue;
+          }
+          const uint8_t* rec = ring + (size_t)s * REC;
+          uint8_t* pp = prep + (size_t)s * L.prep_stride;
+          const uint32_t* kp = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes);
+          const uint32_t* vp = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes + G.kp_bytes);
+          {
+            for (int gr = 0; gr < gpb; ++gr) {
+              uint8_t* qp = pp + gr * QP_BYTES;
+              float za = 0.f, zb = 0.f;  // two chains
+              uint32_t qo[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const int ch = cbk * 32 + 2 * i;
+                const uint2 pr = *reinterpret_cast<const uint2*>(kp + gr * D + ch);
+                const __half2 s2 = u2h(prmt(pr.x, pr.y, 0x5410));
+                const __half2 z2 = u2h(prmt(pr.x, pr.y, 0x7632));
+                qo[i] = h2u(__hmul2(u2h(q2[i]), s2));
+                const float2 zf = __half22float2(z2);
+                za = fmaf(qf[2 * i], zf.x, za);
+                zb = fmaf(qf[2 * i + 1], zf.y, zb);
+              }
+              float zacc = za + zb;
+              uint4* dst = reinterpret_cast<uint4*>(qp + h * QP_ROW + cbk * 64);
+#pragma unroll
+              for (int v = 0; v < 4; ++v)
+                dst[v] = make_uint4(qo[4 * v], qo[4 * v + 1], qo[4 * v + 2], qo[4 * v + 3]);
+              zacc += __shfl_xor_sync(0xffffffffu, zacc, 8);
+              zacc += __shfl_xor_sync(0xffffffffu, zacc, 16);
+              if (cbk == 0) reinterpret_cast<float*>(qp + 8 * QP_ROW)[h] = zacc;
+            }
+          }
+          // per-token V (scale, zero) -> fp32 pairs
+          float2* vsz = reinterpret_cast<float2*>(pp + gpb * QP_BYTES);
+          for (int t = lane; t < G.n_r; t += 32) {
+            const uint32_t pr = vp[t];
+            // token t sits in field position f = field_of_token(t % P), whose
+            // codes enter the MMA as c 2^(sh(f) - 24): fold 2^(SH_REF - sh(f))
+            // into the V scale (B' = P s 2^(SH_REF - sh))
+            const float sv = __half2float(__ushort_as_half((uint16_t)(pr & 0xFFFF)));
+            const int f = field_of_token(t % P, P, G.interleave);
+            vsz[t] = make_float2(sv * exp2f((float)(SH_REF - (f * BITS) % 8)),
+                                 __half2float(__ushort_as_half((uint16_t)(pr >> 16))));
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ready[s]);
+        }
+      }
+      u = seg_end;
+    }
+    return;
+  }
+
+  // ------------------------------------------------------ consumer warps
+  const int grp = warp / WN;  // consumer group: takes blocks it % GRP == grp
+  const int j = warp % WN;    // 16-byte chunk of every channel row
+  const int tok_base = 8 * j * P;
+  const int kgr = G.k_axis == 0 ? tok_base / G.g : 0;
+  const float scale = a.sm_scale_log2;
+  int tok_lab[2 * NPAIR];  // token offset of field position e (labels (g, e))
+#pragma unroll
+  for (int e = 0; e < 2 * NPAIR; ++e) tok_lab[e] = pos_token(e, P, G.interleave);
+  const int stride_slot = slot_stride(ng);
+  const int vsz_off = (G.k_axis == 0 ? G.n_r / G.g : 1) * QP_BYTES;
+
+  int it = 0;
+  long long u = u_begin;
+  for (int cell = cell0; u < u_end; ++cell) {
+    const long long cb = __ldg(a.unit_off + cell), ce = __ldg(a.unit_off + cell + 1);
+    const long long seg_end = min(u_end, ce);
+    const long long res_begin = cb + (long long)__ldg(a.unit_nb + cell);  // 1st residual unit
+    const long long pk_end = min(seg_end, res_begin);
+    Soft st{-INFINITY, -INFINITY, 0.f, 0.f, 0.f, 0.f};
+    float o[OT][4];  // O^T (subnormal-mode scaled, see oscale)
+#pragma unroll
+    for (int mt = 0; mt < OT; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
+
+    // ---------------- packed blocks
+    for (long long x = u; x < pk_end; ++x, ++it) {
+      if (GRP > 1 && (it % GRP) != grp) continue;  // the other group's block
+      const int s = it % NS;
+      unsigned long long tw = 0;
+      if (tr && threadIdx.x == 0) tw = globaltimer();
+      mbar_wait(&ready[s], (it / NS) & 1);
+      mbar_wait(&full[s], (it / NS) & 1);
+      if (tr && threadIdx.x == 0) {
+        const unsigned long long now = globaltimer();
+        if (it == 0) tr[1] = now; else tr[9] += now - tw;
+      }
+      if (a.dev_flags & 1) {  // dev probe: stream only (no compute)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        continue;
+      }
+      const uint8_t* rec = ring + (size_t)s * REC;
+      const uint8_t* pp = prep + (size_t)s * L.prep_stride;
+      const uint8_t* qp = pp + kgr * QP_BYTES;
+      const float2* vsz = reinterpret_cast<const float2*>(pp + vsz_off);
+      // Q'^T B fragments (ldmatrix of the [head][channel] rows)
+      uint32_t qb[KT][2];
+      {
+        const int mi = lane >> 3, r = lane & 7;
+#pragma unroll
+        for (int kk = 0; kk < KT / 2; ++kk) {
+          const int kt = 2 * kk + (mi >> 1);
+          const uint32_t addr = smem_u32(qp + r * QP_ROW + (kt * 16 + (mi & 1) * 8) * 2);
+          ldsm_x4(addr, qb[2 * kk][0], qb[2 * kk][1], qb[2 * kk + 1][0], qb[2 * kk + 1][1]);
+        }
+      }
+      const float2 zz = *reinterpret_cast<const float2*>(qp + 8 * QP_ROW + 8 * t4);
+      const float zs0 = zz.x * scale, zs1 = zz.y * scale;
+
+      // ---- S^T = codes_K . Q'^T over the chunk's 8*P tokens
+      float sacc[NPAIR][4];
+#pragma unroll
+      for (int i = 0; i < NPAIR; ++i) sacc[i][0] = sacc[i][1] = sacc[i][2] = sacc[i][3] = 0.f;
+      {
+        const uint32_t kw = smem_u32(rec);
+        uint32_t kr[4][4];
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) {
+          const int row = kc * 32 + lane;
+          ldsm_x4_t(kw + row * RB + ((j ^ swz(row, WN)) << 4), kr[kc][0], kr[kc][1], kr[kc][2],
+                    kr[kc][3]);
+        }
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const uint32_t rl = kr[kt / 2][2 * (kt % 2)], rh = kr[kt / 2][2 * (kt % 2) + 1];
+          const uint32_t rl8 = rl >> 8, rh8 = rh >> 8;
+#pragma unroll
+          for (int pi = 0; pi < NPAIR; ++pi) {
+            uint32_t af[4];
+#define BDK_KEXT(PI)                                 \
+  if (pi == PI) {                                    \
+    af[0] = ext_sub<BITS, (2 * PI) % P>(rl, rl8);     \
+    af[1] = ext_sub<BITS, (2 * PI + 1) % P>(rl, rl8); \
+    af[2] = ext_sub<BITS, (2 * PI) % P>(rh, rh8);     \
+    af[3] = ext_sub<BITS, (2 * PI + 1) % P>(rh, rh8); \
+  }
+            BDK_KEXT(0)
+            BDK_KEXT(1)
+            BDK_KEXT(2)
+            BDK_KEXT(3)
+#undef BDK_KEXT
+            mma16816(sacc[pi], af, qb[kt][0], qb[kt][1]);
+          }
+        }
+      }
+      // ---- logits (log2 domain), online softmax
+      // S = S' 2^(24 - sh) + Z (rows gid / gid+8 hold fields 2i / 2i+1), in
+      // the log2 domain of the softmax
+#pragma unroll
+      for (int i = 0; i < NPAIR; ++i) {
+        const float al = scale * (float)(1 << (24 - ((2 * i) % P) * BITS % 8));
+        const float ah = scale * (float)(1 << (24 - ((2 * i + 1) % P) * BITS % 8));
+        sacc[i][0] = fmaf(sacc[i][0], al, zs0);
+        sacc[i][1] = fmaf(sacc[i][1], al, zs1);
+        sacc[i][2] = fmaf(sacc[i][2], ah, zs0);
+        sacc[i][3] = fmaf(sacc[i][3], ah, zs1);
+      }
+      softmax_update<NPAIR>(sacc, st, o);
+      // ---- P' = P * s_t (V token scale folded), zero term, P'^T fragments
+      uint32_t pb[NPAIR][2];
+#pragma unroll
+      for (int i = 0; i < NPAIR; ++i) {
+        const int g0 = (8 * j + gid) * P;
+        const float2 sz0 = vsz[g0 + tok_lab[2 * i]];
+        const float2 sz1 = vsz[g0 + tok_lab[2 * i + 1]];
+        st.z0 = fmaf(sacc[i][0], sz0.y, fmaf(sacc[i][2], sz1.y, st.z0));
+        st.z1 = fmaf(sacc[i][1], sz0.y, fmaf(sacc[i][3], sz1.y, st.z1));
+        pb[i][0] = movmatrix_t(pack_h2(sacc[i][0] * sz0.x, sacc[i][1] * sz0.x));
+        pb[i][1] = movmatrix_t(pack_h2(sacc[i][2] * sz1.x, sacc[i][3] * sz1.x));
+      }
+      // ---- O^T += codes_V^T . P'^T
+      {
+        const uint32_t vw = smem_u32(rec + G.wbytes);
+        uint32_t vr[4][4];
+#pragma unroll
+        for (int vc = 0; vc < 4; ++vc) {
+          const int row = vc * 32 + lane;
+          ldsm_x4(vw + row * RB + ((j ^ swz(row, WN)) << 4), vr[vc][0], vr[vc][1], vr[vc][2],
+                  vr[vc][3]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);  // ring slot + prep slot are free
+#pragma unroll
+        for (int mt = 0; mt < KT; ++mt) {
+          const uint32_t ra = vr[mt / 2][2 * (mt % 2)], rb = vr[mt / 2][2 * (mt % 2) + 1];
+          const uint32_t ra8 = ra >> 8, rb8 = rb >> 8;
+#pragma unroll
+          for (int pi = 0; pi < NPAIR; ++pi) {
+            uint32_t af[4];
+#define BDK_VEXT(PI)                                 \
+  if (pi == PI) {                                    \
+    af[0] = ext_sub<BITS, (2 * PI) % P>(ra, ra8);     \
+    af[1] = ext_sub<BITS, (2 * PI) % P>(rb, rb8);     \
+    af[2] = ext_sub<BITS, (2 * PI + 1) % P>(ra, ra8); \
+    af[3] = ext_sub<BITS, (2 * PI + 1) % P>(rb, rb8); \
+  }
+            BDK_VEXT(0)
+            BDK_VEXT(1)
+            BDK_VEXT(2)
+            BDK_VEXT(3)
+#undef BDK_VEXT
+            mma16816(o[mt], af, pb[pi][0], pb[pi][1]);
+          }
+        }
+      }
+    }
+
+    if (tr && threadIdx.x == 0) tr[2] = globaltimer();
+    // ---------------- residual window (fp16), append fused.  Residual unit r
+    // of a cell covers tokens [r*RT, (r+1)*RT) (RT = 16 per consumer warp);
+    // the CTA whose range holds row res_len writes the new token there.
+    int res_app = -1;  // res_len before the append, if this CTA appended
+    float oscale_seg = oscale;
+    if (seg_end > res_begin && !a.skip_residual) {
+      // the packed-block O is held at scale 2^(SH_REF - 24) (subnormal-mode
+      // V codes); the residual V is plain fp16: bring O to unit scale first
+#pragma unroll
+      for (int mt = 0; mt < KT; ++mt) {
+        o[mt][0] *= oscale;
+        o[mt][1] *= oscale;
+        o[mt][2] *= oscale;
+        o[mt][3] *= oscale;
+      }
+      oscale_seg = 1.f;
+      constexpr int RT = 16 * NC;
+      const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
+      __half* rk = c.res_k + (size_t)cell * G.n_r * D;
+      __half* rv = c.res_v + (size_t)cell * G.n_r * D;
+      const int rl0 = c.res_len[cell];
+      const bool app = a.k_new != nullptr;
+      const int rlen = rl0 + (app ? 1 : 0);
+      const int t_lo = (int)(max(u, res_begin) - res_begin) * RT;
+      const int t_hi = min(rlen, (int)(seg_end - res_begin) * RT);
+      if (app && rl0 >= t_lo && rl0 < t_hi) {  // append_token (kvcache.cpp:170-182)
+        const __half* kn = a.k_new + (size_t)cell * D;
+        const __half* vn = a.v_new + (size_t)cell * D;
+        for (int i = threadIdx.x; i < D; i += NC * 32) {
+          rk[(size_t)rl0 * D + i] = kn[i];
+          rv[(size_t)rl0 * D + i] = vn[i];
+        }
+        named_bar(1, NC * 32);
+        res_app = rl0;
+      }
+      uint32_t qb[KT][2];
+      {
+        const __half* qh = a.q + ((size_t)bidx * a.heads_q + (size_t)hk * ng + gid) * D;
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          qb[kt][0] = gid < ng ? *reinterpret_cast<const uint32_t*>(qh + kt * 16 + 2 * t4) : 0u;
+          qb[kt][1] = gid < ng ? *reinterpret_cast<const uint32_t*>(qh + kt * 16 + 8 + 2 * t4) : 0u;
+        }
+      }
+      for (int t0 = t_lo + 16 * warp; t0 < t_hi; t0 += RT) {
+        const bool v0 = t0 + gid < t_hi, v1 = t0 + gid + 8 < t_hi;
+        const __half* k0 = rk + (size_t)(t0 + gid) * D + 2 * t4;
+        const __half* k1 = k0 + 8 * D;
+        float sacc[1][4] = {{0.f, 0.f, 0.f, 0.f}};
+        uint32_t ka[KT][4];
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          ka[kt][0] = v0 ? *reinterpret_cast<const uint32_t*>(k0 + kt * 16) : 0u;
+          ka[kt][1] = v1 ? *reinterpret_cast<const uint32_t*>(k1 + kt * 16) : 0u;
+          ka[kt][2] = v0 ? *reinterpret_cast<const uint32_t*>(k0 + kt * 16 + 8) : 0u;
+          ka[kt][3] = v1 ? *reinterpret_cast<const uint32_t*>(k1 + kt * 16 + 8) : 0u;
+        }
+        // V rows in the natural [token][channel] fragment; movmatrix.trans
+        // turns each 8x8 block into the V^T A-fragment (channel rows)
+        const __half* w0 = rv + (size_t)(t0 + gid) * D + 2 * t4;
+        const __half* w1 = w0 + 8 * D;
+        uint32_t va[KT][4];
+#pragma unroll
+        for (int mt = 0; mt < KT; ++mt) {
+          va[mt][0] = v0 ? *reinterpret_cast<const uint32_t*>(w0 + mt * 16) : 0u;
+          va[mt][1] = v0 ? *reinterpret_cast<const uint32_t*>(w0 + mt * 16 + 8) : 0u;
+          va[mt][2] = v1 ? *reinterpret_cast<const uint32_t*>(w1 + mt * 16) : 0u;
+          va[mt][3] = v1 ? *reinterpret_cast<const uint32_t*>(w1 + mt * 16 + 8) : 0u;
+        }
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) mma16816(sacc[0], ka[kt], qb[kt][0], qb[kt][1]);
+        sacc[0][0] = v0 ? sacc[0][0] * scale : -INFINITY;
+        sacc[0][1] = v0 ? sacc[0][1] * scale : -INFINITY;
+        sacc[0][2] = v1 ? sacc[0][2] * scale : -INFINITY;
+        sacc[0][3] = v1 ? sacc[0][3] * scale : -INFINITY;
+        softmax_update<1>(sacc, st, o);
+        const uint32_t pb0 = movmatrix_t(pack_h2(sacc[0][0], sacc[0][1]));
+        const uint32_t pb1 = movmatrix_t(pack_h2(sacc[0][2], sacc[0][3]));
+#pragma unroll
+        for (int mt = 0; mt < KT; ++mt) {
+          uint32_t af[4];
+          af[0] = movmatrix_t(va[mt][0]);
+          af[1] = movmatrix_t(va[mt][1]);
+          af[2] = movmatrix_t(va[mt][2]);
+          af[3] = movmatrix_t(va[mt][3]);
+          mma16816(o[mt], af, pb0, pb1);
+        }
+      }
+    }
+
+    // ---------------- segment partial -> slot (CTA + cell), completion count
+    if (tr && threadIdx.x == 0) tr[3] = globaltimer();
+    float* slot = a.slots + (size_t)(blockIdx.x + cell) * stride_slot;
+    finalize_segment<NC>(st, o, merge_sm, ng, slot, oscale_seg);  // ends with a barrier
+    if (tr && threadIdx.x == 0) tr[4] = globaltimer();
+    const int lo = cta_of_unit(cb, T, N), hi = cta_of_unit(ce - 1, T, N);
+    if (threadIdx.x == 0) {
+      // release the slot writes of all consumer threads (ordered before this
+      // thread by the barrier) and acquire the other contributors' slots
+      const int prev = atom_add_acq_rel_gpu(a.counters + cell, 1);
+      const int last = prev == hi - lo;
+      if (last) {
+        a.counters[cell] = 0;
+        // commit the append once every contributor has read res_len
+        if (a.k_new != nullptr && !a.skip_residual) c.res_len[cell] = c.res_len[cell] + 1;
+      }
+      *flag = last;
+    }
+    named_bar(1, NC * 32);
+    if (*flag) merge_cell<NC>(a, G, cell, lo, hi, merge_sm);
+    if (tr && threadIdx.x == 0) {
+      tr[5] = globaltimer();
+      tr[6] = (unsigned long long)(*flag);
+      tr[7] = (unsigned long long)(u_end - u_begin);
+      unsigned int smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tr[8] = smid;
+    }
+    named_bar(1, NC * 32);  // flag / merge smem reuse by the next segment
+    u = seg_end;
+  }
+}
+
+}  // namespace
+
+bool fast_decode_ok(const Geom& G, int n_group) {
+  if (G.d != D || n_group < 1 || n_group > 8) return false;
+  if (!(G.bits == 2 || G.bits == 4 || G.bits == 8)) return false;
+  if (!(G.warp_n == 1 || G.warp_n == 2 || G.warp_n == 4 || G.warp_n == 8)) return false;
+  if (G.k_axis != 0) return false;
+  if (G.g != D) return false;  // V: one (scale, zero) per token
+  if (G.n_r % G.g != 0) return false;       // KChannel groups tile the block
+  if (G.g % (8 * G.pack) != 0) return false;  // a warp's chunk lies in one K group
+  return true;
+}
+
+// Variant table: (bits, warp_n) -> kernel with its ring depth and the CTAs
+// per SM it is built for.  BDK_FAST_VARIANT (env, dev knob) picks an
+// alternative ring/occupancy point for the W_n = 4 kernels.
+struct Variant {
+  const void* fn;
+  int ns, grp;
+};
+
+template <int BITS, int WN, int NS, int MINB, int GRP>
+static Variant variant() {
+  return Variant{reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP>), NS,
+                 GRP};
+}
+
+static int variant_knob() {
+  static int v = [] {
+    const char* e = getenv("BDK_FAST_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// default: two co-resident CTAs per SM, one consumer group each, 4-stage ring
+// (measured best on B200); knob 2 = one CTA per SM with two consumer groups
+// over an 8-stage ring (balanced finish, lower throughput), 3 = three groups.
+static Variant fast_kernel(const Geom& G) {
+  const int v = variant_knob();
+#define BDK_SEL(B, W, NS, MB, GR) \
+  if (G.bits == B && G.warp_n == W) return variant<B, W, NS, MB, GR>();
+  if (v == 2) {
+    BDK_SEL(2, 4, 8, 1, 2) BDK_SEL(4, 4, 8, 1, 2)
+  } else if (v == 3) {
+    BDK_SEL(2, 4, 6, 1, 3) BDK_SEL(4, 4, 9, 1, 3)
+  }
+  BDK_SEL(2, 1, 4, 2, 1) BDK_SEL(2, 2, 4, 2, 1) BDK_SEL(2, 4, 4, 2, 1) BDK_SEL(2, 8, 4, 1, 1)
+  BDK_SEL(4, 1, 4, 2, 1) BDK_SEL(4, 2, 4, 2, 1) BDK_SEL(4, 4, 4, 2, 1) BDK_SEL(4, 8, 4, 1, 1)
+  BDK_SEL(8, 1, 4, 2, 1) BDK_SEL(8, 2, 4, 2, 1) BDK_SEL(8, 4, 4, 2, 1) BDK_SEL(8, 8, 4, 1, 1)
+#undef BDK_SEL
+  return Variant{nullptr, 0, 1};
+}
+
+static int fast_threads(const Geom& G, int grp) { return (G.warp_n * grp + 1 + grp) * 32; }
+
+int fast_residual_tokens(const Geom& G) { return 16 * G.warp_n * fast_kernel(G).grp; }
+
+int fast_decode_ctas_per_sm(const Geom& G, int n_group) {
+  const Variant k = fast_kernel(G);
+  if (!k.fn) return 0;
+  const Smem L = smem_layout(G, n_group, k.ns, k.grp);
+  if (cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) !=
+      cudaSuccess)
+    return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k.fn, fast_threads(G, k.grp), L.total) !=
+      cudaSuccess)
+    return 0;
+  return n;
+}
+
+cudaError_t launch_decode_fast(const DevCache& c, const FastArgs& a, cudaStream_t s) {
+  const Variant k = fast_kernel(c.G);
+  if (!k.fn) return cudaErrorInvalidValue;
+  const Smem L = smem_layout(c.G, a.n_group, k.ns, k.grp);
+  DevCache cc = c;
+  FastArgs aa = a;
+  void* args[] = {&cc, &aa};
+  if (a.ev_begin) cudaEventRecord(a.ev_begin, s);
+  cudaError_t e =
+      cudaLaunchKernel(k.fn, dim3(a.n_ctas), dim3(fast_threads(c.G, k.grp)), args, L.total, s);
+  if (e != cudaSuccess) return e;
+  if (a.ev_end) cudaEventRecord(a.ev_end, s);
+  return cudaSuccess;
+}
+
+}  // namespace bdk

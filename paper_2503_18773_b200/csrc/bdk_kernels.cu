@@ -33,6 +33,7 @@
 #include <cfloat>
 
 #include "bdk_launch.h"
+#include "bdk_frag.cuh"
 #include "bdk_qpack.cuh"
 
 namespace bdk {
@@ -81,6 +82,25 @@ template <int BITS>
 __global__ void __launch_bounds__(256) flush_kernel(DevCache c, int cell) {
   extern __shared__ __align__(128) uint8_t smem[];
   const Geom& G = c.G;
+  const int slot = c.packed_blocks[cell];
+  uint8_t* rec = c.records + ((size_t)cell * G.max_blocks + slot) * G.rec_bytes;
+  const size_t base = (size_t)cell * G.n_r * G.d;
+  qpack_block<BITS>(G, c.res_k + base, c.res_v + base, G.d, rec, smem);
+  if (threadIdx.x == 0) {
+    c.packed_blocks[cell] = slot + 1;
+    c.res_len[cell] = 0;
+  }
+}
+
+// flush of every residual that the step filled (decode_step's build_block +
+// commit_block, attention.cpp:103, :235-240): one CTA per cell, no-op unless
+// res_len == N_r
+template <int BITS>
+__global__ void __launch_bounds__(256) flush_full_kernel(DevCache c) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const Geom& G = c.G;
+  const int cell = blockIdx.x;
+  if (c.res_len[cell] != G.n_r) return;
   const int slot = c.packed_blocks[cell];
   uint8_t* rec = c.records + ((size_t)cell * G.max_blocks + slot) * G.rec_bytes;
   const size_t base = (size_t)cell * G.n_r * G.d;
@@ -146,37 +166,6 @@ struct Cfg {
   static constexpr int KT = D / 16;                // 16-channel tiles
 };
 
-template <int SHIFT>
-struct MagicConst {
-  // fp16 bits of 2^-SHIFT and of -1024 * 2^-SHIFT, duplicated in both halves
-  static constexpr uint32_t scale_h = static_cast<uint32_t>(15 - SHIFT) << 10;
-  static constexpr uint32_t bias_h = 0x8000u | (static_cast<uint32_t>(25 - SHIFT) << 10);
-  static constexpr uint32_t scale2 = scale_h | (scale_h << 16);
-  static constexpr uint32_t bias2 = bias_h | (bias_h << 16);
-};
-
-// Code at bit position POS of both 16-bit halves of r as an exact fp16 pair.
-// lop3 ORs the field into the mantissa of 1024.0 (0x6400); the power-of-two
-// rescale is exact, so the result equals the integer code.
-template <int BITS, int POS>
-__device__ __forceinline__ __half2 ext(uint32_t r, uint32_t r8) {
-  if constexpr (BITS == 16) {
-    return u2h(r);
-  } else {
-    constexpr int PB = 8 / BITS;  // fields per byte
-    constexpr int SUB = POS % PB;
-    const uint32_t src = (POS / PB) ? r8 : r;
-    constexpr uint32_t MASK = (((1u << BITS) - 1u) * 0x00010001u) << (SUB * BITS);
-    const uint32_t x = lop3_and_or(src, MASK, 0x64006400u);
-    if constexpr (SUB == 0) {
-      return __hsub2(u2h(x), u2h(0x64006400u));
-    } else {
-      using M = MagicConst<SUB * BITS>;
-      return __hfma2(u2h(x), u2h(M::scale2), u2h(M::bias2));
-    }
-  }
-}
-
 struct SoftState {
   float m0, m1;  // running max (log2 domain) of heads 2*t4, 2*t4+1
   float l0, l1;  // thread-partial exp sums
@@ -241,9 +230,6 @@ __device__ __forceinline__ void softmax_step(float (&s)[NPAIR][4], SoftState& st
   }
 }
 
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
-}
 
 // Per-warp state -> shared -> merged CTA partial (unnormalized O, m, l).
 template <int D, int NW>
@@ -324,7 +310,7 @@ __global__ void __launch_bounds__(Cfg<BITS, D, WN>::NT, 3)
 
   // ===================================================== part 0: residual
   if (part == 0) {
-    const int rl0 = c.res_len[cell];
+    const int rl0 = a.skip_residual ? 0 : c.res_len[cell];
     const int slot = c.packed_blocks[cell];
     __half* rk = c.res_k + (size_t)cell * G.n_r * D;
     __half* rv = c.res_v + (size_t)cell * G.n_r * D;
@@ -787,6 +773,26 @@ cudaError_t launch_flush(const DevCache& c, int cell, cudaStream_t s) {
     case 4: return flush_bits<4>(c, cell, s);
     case 8: return flush_bits<8>(c, cell, s);
     case 16: return flush_bits<16>(c, cell, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int BITS>
+static cudaError_t flush_full_bits(const DevCache& c, cudaStream_t s) {
+  const size_t smem = (size_t)c.G.n_r * c.G.d;
+  auto kern = flush_full_kernel<BITS>;
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), smem);
+  if (e != cudaSuccess) return e;
+  kern<<<c.G.batch * c.G.heads_kv, 256, smem, s>>>(c);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flush_full(const DevCache& c, cudaStream_t s) {
+  switch (c.G.bits) {
+    case 2: return flush_full_bits<2>(c, s);
+    case 4: return flush_full_bits<4>(c, s);
+    case 8: return flush_full_bits<8>(c, s);
+    case 16: return flush_full_bits<16>(c, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -31,13 +31,52 @@ struct DecodeArgs {
   int n_splits = 1, blocks_per_split = 1;
   int blk_begin = 0, blk_end = 1 << 30;  // packed block range attended
   int precise = 0;                        // hi/lo split P
+  int skip_residual = 0;                  // partial decode without the residual
   float sm_scale_log2 = 0.f;
   // optional CUDA events recorded on the launching stream immediately before
   // and after the attention kernel (bdk_profile_begin/end)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
 };
 
+// Fast decode (bdk_decode_fast.cu): stream-K over (cell, unit) with unit =
+// one packed block or the residual window of a cell; in-kernel LSE combine.
+struct FastArgs {
+  const __half* q = nullptr;      // [batch][heads_q][d]
+  const __half* k_new = nullptr;  // [batch][heads_kv][d] (nullptr: no append)
+  const __half* v_new = nullptr;
+  float* out = nullptr;      // [batch][heads_q][d]
+  float* out_lse = nullptr;  // optional [batch][heads_q] (log2 domain)
+  float* slots = nullptr;    // [n_ctas + cells][n_group][d + 2] partials
+  int* counters = nullptr;   // [cells], zero between launches
+  const int* unit_off = nullptr;  // [cells + 1] prefix sum of units per cell
+  const int* unit_nb = nullptr;   // [cells] packed-block units of each cell (the
+                                  // rest are residual units of 16*warp_n tokens)
+  long long total_units = 0;
+  int n_ctas = 0, heads_q = 0, n_group = 0, blk_begin = 0;
+  int skip_residual = 0;  // residual units attend nothing (sequence-split ranks)
+  float sm_scale_log2 = 0.f;
+  unsigned long long* trace = nullptr;  // dev: [n_ctas][16] globaltimer stamps
+  int dev_flags = 0;                    // dev probes (BDK_DEV_FLAGS): 1 no compute, 2 no prep
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+};
+
+// floats per partial slot of the fast kernel: n_group x [d] unnormalized O,
+// then n_group (max, sum) pairs; padded to a float4 multiple
+__host__ __device__ inline int slot_stride(int n_group) {
+  return (n_group * 130 + 3) / 4 * 4;
+}
+
 bool fast_path_ok(const Geom& G);
+// geometry served by the folded-dequant stream-K kernel
+bool fast_decode_ok(const Geom& G, int n_group);
+// resident CTAs per SM of the fast kernel for this geometry (occupancy API)
+int fast_decode_ctas_per_sm(const Geom& G, int n_group);
+// tokens per residual unit of the fast kernel's schedule
+int fast_residual_tokens(const Geom& G);
+cudaError_t launch_decode_fast(const DevCache& c, const FastArgs& a, cudaStream_t s);
+// quantize+pack every full residual window into its next block slot and
+// commit (packed_blocks++, res_len = 0): Algorithm 2's flush after the step
+cudaError_t launch_flush_full(const DevCache& c, cudaStream_t s);
 int max_ctas_per_sm(const Geom& G);
 
 cudaError_t launch_prefill(const DevCache& c, const __half* k, const __half* v, int len,

@@ -194,3 +194,98 @@ def test_host_api_matches_device_api():
                         torch.from_numpy(kn).cuda().half(),
                         torch.from_numpy(vn).cuda().half()).data.cpu().numpy()
     assert np.array_equal(oh, od)
+
+
+# ------------------------------------------- golden fixtures (reference engine)
+@pytest.mark.parametrize("name", ["decode_4bit_gqa", "decode_2bit_wn4_flush", "decode_16bit"])
+@pytest.mark.parametrize("precise", [False, True])
+def test_decode_matches_reference_golden(name, precise):
+    """GPU decode vs decode_step outputs of the UNMODIFIED reference
+    (tests/golden, make_golden.py); inputs regenerated from GaussianSource."""
+    import os
+    bk = _bk()
+    from oracle import oracle as O
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", name + ".npz"))
+    batch, hq, hkv, seq, bits, wn, g, axis, steps, seed = z["meta"].tolist()
+    gauss = O.Gauss(seed)
+    gc = bk.KVCache(batch, hkv, D, wn, bk.QuantSpec(bits, bk.QuantAxis(axis), g),
+                    max_tokens=seq + steps + 512)
+    gc.set_precise(precise)
+    for b in range(batch):
+        for h in range(hkv):
+            k = gauss.rounded(seq * D).reshape(seq, D)
+            v = gauss.rounded(seq * D).reshape(seq, D)
+            gc.prefill(b, h, k, v)
+    cfg = bk.AttentionConfig(batch=batch, heads_q=hq, heads_kv=hkv, head_dim=D, warp_n=wn)
+    for s in range(steps):
+        got = bk.decode_step(gc, cfg, torch.from_numpy(z["q"][s]).cuda().half(),
+                             torch.from_numpy(z["k_new"][s]).cuda().half(),
+                             torch.from_numpy(z["v_new"][s]).cuda().half()).data.cpu().numpy()
+        check_tol(errors(got, z["out"][s]), precise)
+
+
+def test_decode_uneven_cell_lengths():
+    """Cells of different lengths (per-cell prefill): the stream-K schedule
+    spans cell boundaries at arbitrary points."""
+    bk = _bk()
+    from oracle import oracle as O
+    g = O.Gauss(31)
+    hq, hkv, batch, n_r = 16, 4, 3, 128
+    lens = [5 * n_r + 3, 17, 0, 9 * n_r, 2 * n_r - 1, 3 * n_r + 64, 1, 128, 700, 1000, 40, 4 * n_r]
+    oc = O.OracleCache(batch, hkv, D, 4, 4, 0, 128, True, max_tokens=max(lens) + 64)
+    gc = bk.KVCache(batch, hkv, D, 4, bk.QuantSpec(4, bk.QuantAxis.KChannel, 128),
+                    max_tokens=max(lens) + 64)
+    for i, L in enumerate(lens):
+        b, h = divmod(i, hkv)
+        k = g.rounded(L * D).reshape(L, D)
+        v = g.rounded(L * D).reshape(L, D)
+        oc.prefill(b, h, k, v)
+        gc.prefill(b, h, k, v)
+    cfg = bk.AttentionConfig(batch=batch, heads_q=hq, heads_kv=hkv, head_dim=D, warp_n=4)
+    c = Case(heads_q=hq, heads_kv=hkv, batch=batch)
+    worst = {"max_abs": 0.0, "rel_l2": 0.0}
+    for _ in range(3):
+        q, kn, vn = step_data(c, g)
+        ref = oc.decode_step(q, kn, vn)
+        got = bk.decode_step(gc, cfg, torch.from_numpy(q).cuda().half(),
+                             torch.from_numpy(kn).cuda().half(),
+                             torch.from_numpy(vn).cuda().half()).data.cpu().numpy()
+        e = errors(got, ref)
+        worst = {kk: max(worst[kk], e[kk]) for kk in worst}
+    check_tol(worst, False)
+
+
+@pytest.mark.parametrize("precise", [True, False])
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_partial_ranges_merge_to_full_decode(parts, precise):
+    """Sequence split: decode_partial over block ranges + merge_partials ==
+    full decode (split invariance, test_attention.cpp:312-340: 1e-5 in the
+    precise mode; the fast mode's fp16 P is rounded per split, so its bar is
+    the fast tolerance)."""
+    bk = _bk()
+    from oracle import oracle as O
+    from paper_2503_18773_b200 import sharding
+    c = Case(bits=4, warp_n=4, heads_q=32, heads_kv=8, batch=1, prefill=40 * 128 + 77, seed=5)
+    g = O.Gauss(c.seed)
+    k, v = prefill_data(c, g)
+    gc = gpu_cache(c, k, v)
+    gc.set_precise(precise)
+    cfg = bk.AttentionConfig(batch=1, heads_q=32, heads_kv=8, head_dim=D, warp_n=4)
+    q, _, _ = step_data(c, g)
+    qd = torch.from_numpy(q).cuda().half()
+    full_o, full_lse = bk.decode_partial(gc, cfg, qd)
+    nblk = gc.packed_len(0, 0) // gc.n_r()
+    os_, ls_ = [], []
+    for r in range(parts):
+        lo, hi = sharding.block_range(nblk, parts, r)
+        # the residual is attended once, by the last part
+        o, lse = bk.decode_partial(gc, cfg, qd, None, None, lo, hi,
+                                   include_residual=(r == parts - 1))
+        os_.append(o)
+        ls_.append(lse)
+    merged = bk.merge_partials(torch.stack(os_), torch.stack(ls_))
+    if precise:
+        err = (merged - full_o).abs().max().item()
+        assert err < 1e-5, err
+    else:
+        check_tol(errors(merged.cpu().numpy(), full_o.cpu().numpy()), False)

@@ -1,0 +1,46 @@
+"""Summarize an ncu report: key throughput metrics + stall reasons (dev tool)."""
+import csv
+import subprocess
+import sys
+
+KEYS = ['Kernel Name', 'gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+        'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed',
+        'sm__throughput.avg.pct_of_peak_sustained_elapsed',
+        'sm__warps_active.avg.pct_of_peak_sustained_active', 'launch__registers_per_thread',
+        'launch__grid_size', 'launch__block_size', 'launch__occupancy_limit_registers',
+        'launch__occupancy_limit_shared_mem', 'sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active',
+        'sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active',
+        'sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active',
+        'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active',
+        'sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active',
+        'sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active',
+        'smsp__issue_active.avg.pct_of_peak_sustained_active', 'smsp__inst_executed.sum',
+        'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum', 'launch__shared_mem_per_block_dynamic',
+        'smsp__warps_eligible.avg.per_cycle_active', 'smsp__warps_active.avg.per_cycle_active',
+        'lts__t_bytes.sum', 'l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum']
+
+
+def main(path):
+    out = subprocess.run(['ncu', '-i', path, '--page', 'raw', '--csv'], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr = rows[0]
+    for r in rows[2:]:
+        for k in KEYS:
+            if k in hdr:
+                print(f"{k} = {r[hdr.index(k)]}")
+        stalls = []
+        for i, h in enumerate(hdr):
+            if h.startswith('smsp__average_warps_issue_stalled_') and h.endswith('per_issue_active.ratio'):
+                try:
+                    v = float(r[i])
+                except ValueError:
+                    continue
+                if v > 0.05:
+                    stalls.append((v, h.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')))
+        print('stalls/issue:', ', '.join(f'{n}={v:.2f}' for v, n in sorted(stalls, reverse=True)))
+        print('---')
+
+
+if __name__ == '__main__':
+    main(sys.argv[1])
