@@ -50,6 +50,7 @@ struct bdk_cache {
   // attention-kernel timing (bdk_profile_begin/end): one event pair per launch
   bool profiling = false;
   mutable uint64_t launches = 0;  // kernels this cache has launched (all entry points)
+  bool blocks_written = true;  // a packed record may have changed since the last decode
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
   size_t events_used = 0;
 };
@@ -257,7 +258,13 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
   // fast launch (synchronizes; never set in measurements)
   static const char* trace_path = getenv("BDK_TRACE");
   static const int dev_flags = getenv("BDK_DEV_FLAGS") ? atoi(getenv("BDK_DEV_FLAGS")) : 0;
+  static const bool pdl_off = getenv("BDK_PDL") && atoi(getenv("BDK_PDL")) == 0;
   a.dev_flags = dev_flags;
+  // PDL: overlap this launch's prologue (and, unless the previous step wrote
+  // a block, its first TMA prefetches) with the tail of the previous kernel
+  a.pdl = pdl_off || a.ev_begin ? 0 : 1;
+  a.prefetch_ok = c->blocks_written ? 0 : 1;
+  c->blocks_written = false;
   unsigned long long* trace = nullptr;
   if (trace_path) {
     BDK_CUDA(cudaMalloc(&trace, (size_t)n_ctas * 16 * 8), "cudaMalloc(trace)");
@@ -287,6 +294,7 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
     if (any_full) {
       BDK_CUDA(bdk::launch_flush_full(c->dev, stream), "flush launch");
       c->launches += 1;
+      c->blocks_written = true;
     }
     for (int i = 0; i < cells; ++i) {
       if (++c->res_len[i] == G.n_r) {
@@ -513,6 +521,7 @@ bdk_status bdk_prefill(bdk_cache* c, uint32_t b, uint32_t h, const void* k, cons
   if (len > 0 && (!k || !v)) return fail(BDK_INVALID_ARGUMENT, "null k/v");
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
   c->launches += 1;
+  c->blocks_written = true;
   BDK_CUDA(bdk::launch_prefill(c->dev, static_cast<const __half*>(k),
                                static_cast<const __half*>(v), static_cast<int>(len), i, 1,
                                as_stream(stream)),
@@ -533,6 +542,7 @@ bdk_status bdk_prefill_all(bdk_cache* c, const void* k, const void* v, uint32_t 
   const int cells = static_cast<int>(c->res_len.size());
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
   c->launches += 1;
+  c->blocks_written = true;
   BDK_CUDA(bdk::launch_prefill(c->dev, static_cast<const __half*>(k),
                                static_cast<const __half*>(v), static_cast<int>(len), 0, cells,
                                as_stream(stream)),
@@ -572,6 +582,7 @@ bdk_status bdk_flush_residual(bdk_cache* c, uint32_t b, uint32_t h, void* stream
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
   c->launches += 1;
   BDK_CUDA(bdk::launch_flush(c->dev, i, as_stream(stream)), "flush launch");
+  c->blocks_written = true;
   c->packed_blocks[i] += 1;
   c->res_len[i] = 0;
   return BDK_OK;
@@ -717,6 +728,7 @@ bdk_status bdk_adopt_block(bdk_cache* c, uint32_t b, uint32_t h, const uint16_t*
                       rec.data(), G.rec_bytes, cudaMemcpyHostToDevice),
            "H2D block");
   const int nb = slot + 1;
+  c->blocks_written = true;
   BDK_CUDA(cudaMemcpy(c->dev.packed_blocks + i, &nb, sizeof(int), cudaMemcpyHostToDevice),
            "H2D length");
   c->packed_blocks[i] = nb;
@@ -775,6 +787,7 @@ bdk_status bdk_corrupt_word(bdk_cache* c, uint32_t b, uint32_t h, uint32_t blk, 
   const Geom& G = c->dev.G;
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
   BDK_CUDA(cudaDeviceSynchronize(), "sync");
+  const_cast<bdk_cache*>(c)->blocks_written = true;
   BDK_CUDA(cudaMemcpy(c->dev.records + ((size_t)i * G.max_blocks + blk) * G.rec_bytes +
                           word_offset(G, word),
                       &value, 2, cudaMemcpyHostToDevice),

@@ -192,6 +192,13 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
+// programmatic dependent launch (PDL): let the next kernel in the stream start
+// launching / wait until the previous kernel's memory is visible
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -75,7 +75,7 @@ __host__ __device__ inline Smem smem_layout(const Geom& G, int ng, int NS, int g
   Smem L;
   const int gpb = G.k_axis == 0 ? G.n_r / G.g : 1;
   L.ring = 0;
-  L.prep_stride = (uint32_t)(((gpb * QP_BYTES + G.n_r * 8) + 127) / 128 * 128);
+  L.prep_stride = (uint32_t)((gpb * QP_BYTES + 127) / 128 * 128);
   L.prep = L.ring + NS * G.rec_bytes;
   L.merge = L.prep + NS * L.prep_stride;
   const uint32_t merge_bytes =
@@ -324,6 +324,110 @@ __device__ void merge_cell(const FastArgs& a, const Geom& G, int cell, int cta_l
   }
 }
 
+struct PrepCtx {
+  const uint8_t* ring;
+  uint8_t* prep;
+  uint64_t* full;
+  uint64_t* ready;
+  unsigned long long* tr;
+  int rec, prep_stride, pgrp;
+  long long u_begin, u_end;
+  int cell0;
+};
+
+// Prep warp: per packed block of its consumer group, fold the channel-wise K
+// scales into the query, Q'[h][c] = fp16(q[h][c] s_c), and the zero points
+// into Z[h] = sum_c q[h][c] z_c (fp32), for every K group of the block.
+// NH = n_group rounded up to a power of two: lane -> (head lane % NH, a block
+// of 4*NH channels), so only real heads cost work; Q' rows of heads >= n_group
+// stay zero (prep areas are zeroed at kernel start).
+template <int NH, int NS, int GRP>
+__device__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& px) {
+  constexpr int LPH = 32 / NH;  // lanes per head
+  constexpr int CPL = D / LPH;  // channels per lane
+  constexpr int H2 = CPL / 2;   // half2 per lane
+  const Geom& G = c.G;
+  const int lane = threadIdx.x & 31;
+  const int h = lane % NH, cbk = lane / NH;
+  const int ng = a.n_group;
+  const int gpb = G.k_axis == 0 ? G.n_r / G.g : 1;
+  int it = 0;
+  long long u = px.u_begin;
+  for (int cell = px.cell0; u < px.u_end; ++cell) {
+    const long long ce = __ldg(a.unit_off + cell + 1);
+    const long long seg_end = min(px.u_end, ce);
+    const long long pk_end =
+        min(seg_end, (long long)__ldg(a.unit_off + cell) + __ldg(a.unit_nb + cell));
+    if (u < pk_end) {
+      const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
+      uint32_t q2[H2];
+      float qf[CPL];
+#pragma unroll
+      for (int i = 0; i < H2; ++i) q2[i] = 0u;
+      if (h < ng) {
+        const uint32_t* qs = reinterpret_cast<const uint32_t*>(
+            a.q + ((size_t)bidx * a.heads_q + (size_t)hk * ng + h) * D + cbk * CPL);
+#pragma unroll
+        for (int i = 0; i < H2; ++i) q2[i] = __ldg(qs + i);
+      }
+#pragma unroll
+      for (int i = 0; i < H2; ++i) {
+        const float2 f = __half22float2(u2h(q2[i]));
+        qf[2 * i] = f.x;
+        qf[2 * i + 1] = f.y;
+      }
+      for (long long x = u; x < pk_end; ++x, ++it) {
+        if (GRP > 1 && (it % GRP) != px.pgrp) continue;
+        const int s = it % NS;
+        const unsigned long long tw = (px.tr && lane == 0) ? globaltimer() : 0ull;
+        mbar_wait_sleep(&px.full[s], (it / NS) & 1);
+        const unsigned long long tb = (px.tr && lane == 0) ? globaltimer() : 0ull;
+        if (px.tr && lane == 0) px.tr[12] += tb - tw;
+        if (!(a.dev_flags & 2)) {
+          const uint8_t* rec = px.ring + (size_t)s * px.rec;
+          uint8_t* pp = px.prep + (size_t)s * px.prep_stride;
+          const uint32_t* kp = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes);
+          for (int gr = 0; gr < gpb; ++gr) {
+            uint8_t* qp = pp + gr * QP_BYTES;
+            float za = 0.f, zb = 0.f;
+            uint32_t qo[H2];
+#pragma unroll
+            for (int i = 0; i < H2; ++i) {
+              const uint2 pr = *reinterpret_cast<const uint2*>(kp + gr * D + cbk * CPL + 2 * i);
+              const __half2 s2 = u2h(prmt(pr.x, pr.y, 0x5410));
+              const __half2 z2 = u2h(prmt(pr.x, pr.y, 0x7632));
+              qo[i] = h2u(__hmul2(u2h(q2[i]), s2));
+              const float2 zf = __half22float2(z2);
+              za = fmaf(qf[2 * i], zf.x, za);
+              zb = fmaf(qf[2 * i + 1], zf.y, zb);
+            }
+            if (h < ng) {
+              uint32_t* dst = reinterpret_cast<uint32_t*>(qp + h * QP_ROW + cbk * CPL * 2);
+              if constexpr (H2 % 4 == 0) {
+#pragma unroll
+                for (int v = 0; v < H2 / 4; ++v)
+                  reinterpret_cast<uint4*>(dst)[v] =
+                      make_uint4(qo[4 * v], qo[4 * v + 1], qo[4 * v + 2], qo[4 * v + 3]);
+              } else {
+#pragma unroll
+                for (int v = 0; v < H2; ++v) dst[v] = qo[v];
+              }
+            }
+            float zacc = za + zb;
+#pragma unroll
+            for (int off = NH; off < 32; off <<= 1) zacc += __shfl_xor_sync(0xffffffffu, zacc, off);
+            if (cbk == 0 && h < ng) reinterpret_cast<float*>(qp + 8 * QP_ROW)[h] = zacc;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&px.ready[s]);
+        if (px.tr && lane == 0) px.tr[13] += globaltimer() - tb;
+      }
+    }
+    u = seg_end;
+  }
+}
+
 template <int BITS, int WN, int NS, int MINB, int GRP>
 __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     decode_fast_kernel(DevCache c, FastArgs a) {
@@ -366,6 +470,9 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   const int N = a.n_ctas;
   const long long u_begin = (long long)blockIdx.x * T / N;
   const long long u_end = (long long)(blockIdx.x + 1) * T / N;
+  // PDL: the next kernel may start its own prologue as soon as every CTA of
+  // this one is resident (the grid is one wave, so this cannot starve it)
+  pdl_launch_dependents();
   if (u_begin >= u_end) return;
   const int cell0 = find_cell(a.unit_off, cells, u_begin);
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * 16 : nullptr;
@@ -377,6 +484,14 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       const uint64_t pol = policy_evict_first();
       int it = 0;
       long long u = u_begin;
+      // the first NS records may stream in before the previous kernel ends
+      // (they are immutable unless that kernel was a flush); everything else
+      // waits for its memory to be visible
+      bool waited = !a.pdl;
+      if (!a.prefetch_ok && !waited) {
+        pdl_wait();
+        waited = true;
+      }
       for (int cell = cell0; u < u_end; ++cell) {
         const long long cb = __ldg(a.unit_off + cell), ce = __ldg(a.unit_off + cell + 1);
         const long long seg_end = min(u_end, ce);
@@ -384,7 +499,15 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
         const uint8_t* base = c.records + (size_t)cell * G.max_blocks * REC;
         for (long long x = u; x < pk_end; ++x, ++it) {
           const int s = it % NS;
-          if (it >= NS) mbar_wait_sleep(&empty[s], ((it / NS) - 1) & 1);
+          if (!waited && it == NS) {
+            pdl_wait();
+            waited = true;
+          }
+          if (it >= NS) {
+            const unsigned long long tw = tr ? globaltimer() : 0ull;
+            mbar_wait_sleep(&empty[s], ((it / NS) - 1) & 1);
+            if (tr) tr[11] += globaltimer() - tw;
+          }
           mbar_expect_tx(&full[s], (uint32_t)REC);
           const int blk = a.blk_begin + (int)(x - cb);
           tma_bulk_g2s(ring + (size_t)s * REC, base + (size_t)blk * REC, (uint32_t)REC, &full[s],
@@ -397,100 +520,15 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   }
 
   // ---------------------------------------------------------- prep warps
+  if (a.pdl && warp != NC) pdl_wait();  // q, cache state, counters, slots
   if (warp > NC) {
     const int pgrp = warp - NC - 1;  // prepares the blocks of consumer group pgrp
-    const int gpb = G.k_axis == 0 ? G.n_r / G.g : 1;
-    const int h = lane & 7, cbk = lane >> 3;  // head, 32-channel block
-
-    int it = 0;
-    long long u = u_begin;
-    for (int cell = cell0; u < u_end; ++cell) {
-      const long long ce = __ldg(a.unit_off + cell + 1);
-      const long long seg_end = min(u_end, ce);
-      const long long pk_end =
-          min(seg_end, (long long)__ldg(a.unit_off + cell) + __ldg(a.unit_nb + cell));
-      if (u < pk_end) {
-        const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
-        // lanes of heads >= n_group carry q = 0: they write the zero Q' rows
-        uint32_t q2[16];
-        float qf[32];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) q2[i] = 0u;
-        if (h < ng) {
-          const uint4* qs = reinterpret_cast<const uint4*>(
-              a.q + ((size_t)bidx * a.heads_q + (size_t)hk * ng + h) * D + cbk * 32);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const uint4 w = __ldg(qs + v);
-            q2[4 * v] = w.x;
-            q2[4 * v + 1] = w.y;
-            q2[4 * v + 2] = w.z;
-            q2[4 * v + 3] = w.w;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float2 f = __half22float2(u2h(q2[i]));
-          qf[2 * i] = f.x;
-          qf[2 * i + 1] = f.y;
-        }
-        for (long long x = u; x < pk_end; ++x, ++it) {
-          if (GRP > 1 && (it % GRP) != pgrp) continue;
-          const int s = it % NS;
-          mbar_wait_sleep(&full[s], (it / NS) & 1);
-          if (a.dev_flags & 2) {  // dev probe: no prep work
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&ready[s]);
-            continue;
-          }
-          const uint8_t* rec = ring + (size_t)s * REC;
-          uint8_t* pp = prep + (size_t)s * L.prep_stride;
-          const uint32_t* kp = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes);
-          const uint32_t* vp = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes + G.kp_bytes);
-          {
-            for (int gr = 0; gr < gpb; ++gr) {
-              uint8_t* qp = pp + gr * QP_BYTES;
-              float za = 0.f, zb = 0.f;  // two chains
-              uint32_t qo[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const int ch = cbk * 32 + 2 * i;
-                const uint2 pr = *reinterpret_cast<const uint2*>(kp + gr * D + ch);
-                const __half2 s2 = u2h(prmt(pr.x, pr.y, 0x5410));
-                const __half2 z2 = u2h(prmt(pr.x, pr.y, 0x7632));
-                qo[i] = h2u(__hmul2(u2h(q2[i]), s2));
-                const float2 zf = __half22float2(z2);
-                za = fmaf(qf[2 * i], zf.x, za);
-                zb = fmaf(qf[2 * i + 1], zf.y, zb);
-              }
-              float zacc = za + zb;
-              uint4* dst = reinterpret_cast<uint4*>(qp + h * QP_ROW + cbk * 64);
-#pragma unroll
-              for (int v = 0; v < 4; ++v)
-                dst[v] = make_uint4(qo[4 * v], qo[4 * v + 1], qo[4 * v + 2], qo[4 * v + 3]);
-              zacc += __shfl_xor_sync(0xffffffffu, zacc, 8);
-              zacc += __shfl_xor_sync(0xffffffffu, zacc, 16);
-              if (cbk == 0) reinterpret_cast<float*>(qp + 8 * QP_ROW)[h] = zacc;
-            }
-          }
-          // per-token V (scale, zero) -> fp32 pairs
-          float2* vsz = reinterpret_cast<float2*>(pp + gpb * QP_BYTES);
-          for (int t = lane; t < G.n_r; t += 32) {
-            const uint32_t pr = vp[t];
-            // token t sits in field position f = field_of_token(t % P), whose
-            // codes enter the MMA as c 2^(sh(f) - 24): fold 2^(SH_REF - sh(f))
-            // into the V scale (B' = P s 2^(SH_REF - sh))
-            const float sv = __half2float(__ushort_as_half((uint16_t)(pr & 0xFFFF)));
-            const int f = field_of_token(t % P, P, G.interleave);
-            vsz[t] = make_float2(sv * exp2f((float)(SH_REF - (f * BITS) % 8)),
-                                 __half2float(__ushort_as_half((uint16_t)(pr >> 16))));
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ready[s]);
-        }
-      }
-      u = seg_end;
-    }
+    const int nh = ng <= 1 ? 1 : ng <= 2 ? 2 : ng <= 4 ? 4 : 8;
+    PrepCtx px{ring, prep, full, ready, tr, REC, (int)L.prep_stride, pgrp, u_begin, u_end, cell0};
+    if (nh == 1) prep_loop<1, NS, GRP>(c, a, px);
+    else if (nh == 2) prep_loop<2, NS, GRP>(c, a, px);
+    else if (nh == 4) prep_loop<4, NS, GRP>(c, a, px);
+    else prep_loop<8, NS, GRP>(c, a, px);
     return;
   }
 
@@ -504,7 +542,6 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
 #pragma unroll
   for (int e = 0; e < 2 * NPAIR; ++e) tok_lab[e] = pos_token(e, P, G.interleave);
   const int stride_slot = slot_stride(ng);
-  const int vsz_off = (G.k_axis == 0 ? G.n_r / G.g : 1) * QP_BYTES;
 
   int it = 0;
   long long u = u_begin;
@@ -538,7 +575,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       const uint8_t* rec = ring + (size_t)s * REC;
       const uint8_t* pp = prep + (size_t)s * L.prep_stride;
       const uint8_t* qp = pp + kgr * QP_BYTES;
-      const float2* vsz = reinterpret_cast<const float2*>(pp + vsz_off);
+      const uint32_t* vpr = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes + G.kp_bytes);
       // Q'^T B fragments (ldmatrix of the [head][channel] rows)
       uint32_t qb[KT][2];
       {
@@ -606,9 +643,16 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       uint32_t pb[NPAIR][2];
 #pragma unroll
       for (int i = 0; i < NPAIR; ++i) {
+        // V (scale, zero) of the tokens of rows gid / gid+8 (fields 2i / 2i+1);
+        // the scale carries 2^(SH_REF - sh) of the field's subnormal shift
         const int g0 = (8 * j + gid) * P;
-        const float2 sz0 = vsz[g0 + tok_lab[2 * i]];
-        const float2 sz1 = vsz[g0 + tok_lab[2 * i + 1]];
+        const float2 pa = __half22float2(u2h(vpr[g0 + tok_lab[2 * i]]));
+        const float2 pz = __half22float2(u2h(vpr[g0 + tok_lab[2 * i + 1]]));
+        const float2 sz0 = make_float2(
+            pa.x * (float)(1 << (SH_REF + 8)) / (float)(1 << (8 + ((2 * i) % P) * BITS % 8)), pa.y);
+        const float2 sz1 = make_float2(
+            pz.x * (float)(1 << (SH_REF + 8)) / (float)(1 << (8 + ((2 * i + 1) % P) * BITS % 8)),
+            pz.y);
         st.z0 = fmaf(sacc[i][0], sz0.y, fmaf(sacc[i][2], sz1.y, st.z0));
         st.z1 = fmaf(sacc[i][1], sz0.y, fmaf(sacc[i][3], sz1.y, st.z1));
         pb[i][0] = movmatrix_t(pack_h2(sacc[i][0] * sz0.x, sacc[i][1] * sz0.x));
@@ -855,8 +899,17 @@ cudaError_t launch_decode_fast(const DevCache& c, const FastArgs& a, cudaStream_
   FastArgs aa = a;
   void* args[] = {&cc, &aa};
   if (a.ev_begin) cudaEventRecord(a.ev_begin, s);
-  cudaError_t e =
-      cudaLaunchKernel(k.fn, dim3(a.n_ctas), dim3(fast_threads(c.G, k.grp)), args, L.total, s);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.n_ctas);
+  cfg.blockDim = dim3(fast_threads(c.G, k.grp));
+  cfg.dynamicSmemBytes = L.total;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelExC(&cfg, k.fn, args);
   if (e != cudaSuccess) return e;
   if (a.ev_end) cudaEventRecord(a.ev_end, s);
   return cudaSuccess;

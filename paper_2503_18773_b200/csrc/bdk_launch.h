@@ -57,6 +57,9 @@ struct FastArgs {
   float sm_scale_log2 = 0.f;
   unsigned long long* trace = nullptr;  // dev: [n_ctas][16] globaltimer stamps
   int dev_flags = 0;                    // dev probes (BDK_DEV_FLAGS): 1 no compute, 2 no prep
+  int pdl = 0;          // launched as a programmatic dependent of the previous kernel
+  int prefetch_ok = 0;  // packed records unchanged since the previous kernel: the
+                        // TMA warp may prefetch them before griddepcontrol.wait
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
 };
 

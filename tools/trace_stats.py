@@ -26,6 +26,9 @@ print("merge (last CTAs)", q((a[m, 5] - a[m, 4]) / 1e3), "n=", m.sum())
 print("units/CTA", q(a[:, 7]))
 if a.shape[1] > 9:
     print("cons. wait (ns->us)", q(a[:, 9] / 1e3))
+    print("TMA empty-wait   ", q(a[:, 11] / 1e3))
+    print("prep full-wait   ", q(a[:, 12] / 1e3))
+    print("prep busy        ", q(a[:, 13] / 1e3))
     loop = (a[:, 2] - a[:, 1]) / 1e3
     # per-SM: both CTAs on an SM
     sm = a[:, 8].astype(int)
