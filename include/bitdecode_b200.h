@@ -118,6 +118,17 @@ BDK_API bdk_status bdk_prefill(bdk_cache* cache, uint32_t b, uint32_t h, const v
  * bench.cpp:132-139, in one launch). */
 BDK_API bdk_status bdk_prefill_all(bdk_cache* cache, const void* k_dev, const void* v_dev,
                                    uint32_t len, void* stream);
+/* Host-buffer variants (binary16 bits in host memory; synchronous): the entry
+ * points the C++ drop-in (bitkv_b200.hpp) binds for the reference's
+ * host-pointer API (KVCache::prefill / append_token / packed_tile). */
+BDK_API bdk_status bdk_prefill_host(bdk_cache* cache, uint32_t b, uint32_t h,
+                                    const uint16_t* k_host, const uint16_t* v_host, uint32_t len);
+BDK_API bdk_status bdk_append_token_host(bdk_cache* cache, uint32_t b, uint32_t h,
+                                         const uint16_t* k_row_host, const uint16_t* v_row_host);
+/* KVCache::packed_tile (kvcache.cpp:263-312): dequantized tokens
+ * [t0, t0 + len) of the packed segment, binary16 bits [len][head_dim]. */
+BDK_API bdk_status bdk_packed_tile_host(const bdk_cache* cache, uint32_t b, uint32_t h, uint32_t t0,
+                                        uint32_t len, uint16_t* k_host, uint16_t* v_host);
 /* KVCache::append_token (kvcache.cpp:170-182); rows binary16 [head_dim]. */
 BDK_API bdk_status bdk_append_token(bdk_cache* cache, uint32_t b, uint32_t h,
                                     const void* k_row_dev, const void* v_row_dev, void* stream);

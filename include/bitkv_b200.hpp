@@ -1,0 +1,455 @@
+// bitkv_b200.hpp -- C++20 drop-in for the reference engine's public API
+// (/root/reference/proj/include/bitkv, namespace bitkv) over the sm_100a
+// C-ABI in bitdecode_b200.h.
+//
+// Include this header INSTEAD of the reference headers and link
+// libbitdecode_b200.so: the names, argument meaning, value semantics and
+// exception classes follow the reference (cited per symbol), while the cache
+// lives in HBM and every numeric step -- fused quantize+pack, dequant,
+// decode attention, LSE combine -- runs in the CUDA kernels.  The only code in
+// this header is host bookkeeping: shape checks, status -> exception mapping,
+// and the binary16 <-> fp32 value conversions of the reference Tensor contract
+// (tensor.hpp:16-46, all API values are binary16-representable).
+//
+// Extensions (documented, no reference counterpart): the KVCache constructor
+// takes an optional per-cell token capacity (the device arena is sized once;
+// the reference grows host vectors) and a CUDA device ordinal.
+#pragma once
+
+#include <bit>
+#include <cmath>
+#include <utility>
+#include <cstddef>
+#include <cstdint>
+#include <cstring>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "bitdecode_b200.h"
+
+namespace bitkv {
+
+// ------------------------------------------------------------ errors.hpp
+struct Error : std::runtime_error {  // errors.hpp:9-12
+  using std::runtime_error::runtime_error;
+};
+struct ConfigError : Error {  // errors.hpp:14-54
+  using Error::Error;
+};
+struct ShapeError : Error {
+  using Error::Error;
+};
+struct UnsupportedBits : Error {
+  using Error::Error;
+};
+struct CodeOverflow : Error {
+  using Error::Error;
+};
+struct CapacityError : Error {
+  using Error::Error;
+};
+struct StateError : Error {
+  using Error::Error;
+};
+struct FormatError : Error {
+  using Error::Error;
+};
+struct EmptyInput : Error {
+  using Error::Error;
+};
+struct CudaError : Error {  // device / driver failure (no reference counterpart)
+  using Error::Error;
+};
+struct Unsupported : Error {  // geometry outside the sm_100a kernels' envelope
+  using Error::Error;
+};
+
+namespace detail {
+inline void check(bdk_status s) {
+  if (s == BDK_OK) return;
+  const std::string msg = bdk_last_error();
+  switch (s) {
+    case BDK_CONFIG_ERROR: throw ConfigError(msg);
+    case BDK_SHAPE_ERROR: throw ShapeError(msg);
+    case BDK_UNSUPPORTED_BITS: throw UnsupportedBits(msg);
+    case BDK_CODE_OVERFLOW: throw CodeOverflow(msg);
+    case BDK_CAPACITY_ERROR: throw CapacityError(msg);
+    case BDK_STATE_ERROR: throw StateError(msg);
+    case BDK_FORMAT_ERROR: throw FormatError(msg);
+    case BDK_EMPTY_INPUT: throw EmptyInput(msg);
+    case BDK_CUDA_ERROR: throw CudaError(msg);
+    case BDK_UNSUPPORTED: throw Unsupported(msg);
+    default: throw Error(msg);
+  }
+}
+}  // namespace detail
+
+// -------------------------------------------------------------- fp16.hpp
+// IEEE binary16 <-> binary32 with round-to-nearest-even (fp16.hpp:13-70).
+inline uint16_t f32_to_f16_bits(float value) {
+  return std::bit_cast<uint16_t>(static_cast<_Float16>(value));
+}
+inline float f16_bits_to_f32(uint16_t bits) {
+  return static_cast<float>(std::bit_cast<_Float16>(bits));
+}
+inline float round_f16(float value) { return f16_bits_to_f32(f32_to_f16_bits(value)); }
+
+// ------------------------------------------------------------ tensor.hpp
+class Tensor {  // tensor.hpp:16-81: row-major fp32 storage of binary16 values
+ public:
+  Tensor() = default;
+  explicit Tensor(std::vector<size_t> shape) : shape_(std::move(shape)) {
+    data_.assign(count(shape_), 0.0f);
+  }
+  static Tensor from_values(std::vector<size_t> shape, const std::vector<float>& values) {
+    Tensor t(std::move(shape));
+    if (values.size() != t.data_.size())
+      throw ShapeError("from_values: element count does not match shape");
+    for (size_t i = 0; i < values.size(); ++i) t.data_[i] = round_f16(values[i]);
+    return t;
+  }
+  const std::vector<size_t>& shape() const { return shape_; }
+  size_t ndim() const { return shape_.size(); }
+  size_t dim(size_t i) const { return shape_.at(i); }
+  size_t numel() const { return data_.size(); }
+  float at(size_t flat) const { return data_[flat]; }
+  float operator()(size_t i, size_t j) const { return data_[flat2(i, j)]; }
+  float operator()(size_t i, size_t j, size_t k) const { return data_[flat3(i, j, k)]; }
+  void set(size_t flat, float v) { data_[flat] = round_f16(v); }
+  void set(size_t i, size_t j, float v) { data_[flat2(i, j)] = round_f16(v); }
+  void set(size_t i, size_t j, size_t k, float v) { data_[flat3(i, j, k)] = round_f16(v); }
+  const float* data() const { return data_.data(); }
+  const std::vector<float>& values() const { return data_; }
+
+ private:
+  static size_t count(const std::vector<size_t>& s) {
+    size_t n = 1;
+    for (size_t d : s) n *= d;
+    return n;
+  }
+  size_t flat2(size_t i, size_t j) const {
+    if (shape_.size() != 2) throw ShapeError("2-d index into non-2-d tensor");
+    return i * shape_[1] + j;
+  }
+  size_t flat3(size_t i, size_t j, size_t k) const {
+    if (shape_.size() != 3) throw ShapeError("3-d index into non-3-d tensor");
+    return (i * shape_[1] + j) * shape_[2] + k;
+  }
+  std::vector<size_t> shape_;
+  std::vector<float> data_;
+};
+
+// ------------------------------------------------------------- quant.hpp
+enum class QuantAxis : uint32_t { KChannel = 0, KToken = 1 };  // quant.hpp:12-15
+
+struct QuantSpec {  // quant.hpp:19-25
+  uint32_t num_bits = 4;
+  QuantAxis k_axis = QuantAxis::KChannel;
+  size_t group_size = 64;
+  bool passthrough() const { return num_bits == 16; }
+};
+
+struct QuantParams {  // quant.hpp:38-47: (scale, zero) binary16 pairs
+  size_t rows = 0;
+  size_t cols = 0;
+  std::vector<uint16_t> data;
+  size_t group_count() const { return rows * cols; }
+  float scale(size_t g) const { return f16_bits_to_f32(data[2 * g]); }
+  float zero(size_t g) const { return f16_bits_to_f32(data[2 * g + 1]); }
+  bool operator==(const QuantParams&) const = default;
+};
+
+inline constexpr float kMinScale = 6.103515625e-05f;  // quant.hpp:52
+
+// ------------------------------------------------------------ layout.hpp
+inline size_t residual_block_size(uint32_t num_bits, size_t warp_n) {  // layout.cpp:74-77
+  if (num_bits != 2 && num_bits != 4 && num_bits != 8 && num_bits != 16)
+    throw UnsupportedBits("num_bits must be one of 2, 4, 8, 16");
+  return 8 * warp_n * (16 / num_bits);
+}
+
+// ------------------------------------------------------------ config.hpp
+struct AttentionConfig {  // config.hpp:13-25
+  size_t batch = 1;
+  size_t heads_q = 32;
+  size_t heads_kv = 8;
+  size_t head_dim = 128;
+  size_t tile_m = 1;
+  size_t tile_n = 64;
+  size_t num_splits = 1;
+  size_t warp_n = 4;
+  size_t warp_m = 1;
+  size_t n_group() const { return heads_q / heads_kv; }
+};
+
+namespace detail {
+inline bdk_attn_config to_c(const AttentionConfig& c) {
+  bdk_attn_config o{};
+  o.batch = static_cast<uint32_t>(c.batch);
+  o.heads_q = static_cast<uint32_t>(c.heads_q);
+  o.heads_kv = static_cast<uint32_t>(c.heads_kv);
+  o.head_dim = static_cast<uint32_t>(c.head_dim);
+  o.tile_m = static_cast<uint32_t>(c.tile_m);
+  o.tile_n = static_cast<uint32_t>(c.tile_n);
+  o.num_splits = static_cast<uint32_t>(c.num_splits);
+  o.warp_n = static_cast<uint32_t>(c.warp_n);
+  o.warp_m = static_cast<uint32_t>(c.warp_m);
+  return o;
+}
+}  // namespace detail
+
+inline AttentionConfig validate_config(const AttentionConfig& cfg) {  // config.cpp:10-30
+  const bdk_attn_config c = detail::to_c(cfg);
+  detail::check(bdk_validate_config(&c));
+  return cfg;
+}
+
+// ----------------------------------------------------------- kvcache.hpp
+struct PackedBlock {  // kvcache.hpp:17-26
+  std::vector<uint16_t> k_words;
+  std::vector<uint16_t> v_words;
+  QuantParams k_params;
+  QuantParams v_params;
+  bool operator==(const PackedBlock&) const = default;
+};
+
+struct PackedKV {  // kvcache.hpp:28-43
+  std::vector<PackedBlock> blocks;
+  size_t packed_len = 0;
+};
+
+enum class CacheBackend { Contiguous, Paged };  // kvcache.hpp:100
+
+class KVCache {  // kvcache.hpp:103-189, cache resident in HBM
+ public:
+  KVCache(size_t batch, size_t heads_kv, size_t head_dim, size_t warp_n, QuantSpec spec,
+          CacheBackend backend = CacheBackend::Contiguous, size_t page_size = 16,
+          size_t max_pages = 0, bool interleave = true, size_t max_tokens = 65536,
+          int device = 0)
+      : batch_(batch), heads_kv_(heads_kv), head_dim_(head_dim), warp_n_(warp_n), spec_(spec),
+        backend_(backend), page_size_(page_size), interleave_(interleave) {
+    (void)max_pages;
+    if (backend == CacheBackend::Paged) {
+      const size_t n_r = residual_block_size(spec.num_bits, warp_n);
+      if (page_size == 0 || n_r % page_size != 0)
+        throw ConfigError("page_size must divide N_r");
+    }
+    bdk_cache_desc d{};
+    d.batch = static_cast<uint32_t>(batch);
+    d.heads_kv = static_cast<uint32_t>(heads_kv);
+    d.head_dim = static_cast<uint32_t>(head_dim);
+    d.warp_n = static_cast<uint32_t>(warp_n);
+    d.num_bits = spec.num_bits;
+    d.k_axis = static_cast<uint32_t>(spec.k_axis);
+    d.group_size = static_cast<uint32_t>(spec.group_size);
+    d.interleave = interleave ? 1u : 0u;
+    d.max_tokens = static_cast<uint32_t>(max_tokens);
+    d.device = device;
+    detail::check(bdk_cache_create(&d, &h_));
+    detail::check(bdk_cache_get_info(h_, &info_));
+  }
+  KVCache(const KVCache&) = delete;
+  KVCache& operator=(const KVCache&) = delete;
+  KVCache(KVCache&& o) noexcept { *this = std::move(o); }
+  KVCache& operator=(KVCache&& o) noexcept {
+    std::swap(h_, o.h_);
+    batch_ = o.batch_;
+    heads_kv_ = o.heads_kv_;
+    head_dim_ = o.head_dim_;
+    warp_n_ = o.warp_n_;
+    spec_ = o.spec_;
+    backend_ = o.backend_;
+    page_size_ = o.page_size_;
+    interleave_ = o.interleave_;
+    info_ = o.info_;
+    return *this;
+  }
+  ~KVCache() {
+    if (h_) bdk_cache_destroy(h_);
+  }
+
+  size_t batch() const { return batch_; }
+  size_t heads_kv() const { return heads_kv_; }
+  size_t head_dim() const { return head_dim_; }
+  size_t warp_n() const { return warp_n_; }
+  size_t n_r() const { return info_.n_r; }
+  const QuantSpec& spec() const { return spec_; }
+  CacheBackend backend() const { return backend_; }
+  size_t page_size() const { return page_size_; }
+  bool interleaved() const { return interleave_; }
+  bdk_cache* handle() const { return h_; }
+
+  // KVCache::prefill (kvcache.cpp:155-168): fused quantize+pack on device
+  void prefill(size_t b, size_t h, const float* k, const float* v, size_t len) {
+    std::vector<uint16_t> kb(len * head_dim_), vb(len * head_dim_);
+    for (size_t i = 0; i < kb.size(); ++i) {
+      kb[i] = f32_to_f16_bits(k[i]);
+      vb[i] = f32_to_f16_bits(v[i]);
+    }
+    detail::check(bdk_prefill_host(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h),
+                                   kb.data(), vb.data(), static_cast<uint32_t>(len)));
+  }
+  // KVCache::append_token (kvcache.cpp:170-182)
+  void append_token(size_t b, size_t h, const float* k_row, const float* v_row) {
+    std::vector<uint16_t> kb(head_dim_), vb(head_dim_);
+    for (size_t i = 0; i < head_dim_; ++i) {
+      kb[i] = f32_to_f16_bits(k_row[i]);
+      vb[i] = f32_to_f16_bits(v_row[i]);
+    }
+    detail::check(bdk_append_token_host(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h),
+                                        kb.data(), vb.data()));
+  }
+  // KVCache::flush_residual (kvcache.cpp:245-251)
+  void flush_residual(size_t b, size_t h) {
+    detail::check(
+        bdk_flush_residual(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h), nullptr));
+    detail::check(bdk_synchronize());
+  }
+  // KVCache::adopt_block (kvcache.cpp:239-243)
+  void adopt_block(size_t b, size_t h, const PackedBlock& blk) {
+    detail::check(bdk_adopt_block(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h),
+                                  blk.k_words.data(), blk.v_words.data(),
+                                  blk.k_params.data.data(), blk.v_params.data.data()));
+  }
+
+  size_t packed_len(size_t b, size_t h) const { return lengths(b, h).first; }
+  size_t res_len(size_t b, size_t h) const { return lengths(b, h).second; }
+  size_t total_len(size_t b, size_t h) const {
+    const auto l = lengths(b, h);
+    return l.first + l.second;
+  }
+
+  // KVCache::packed(b, h) (kvcache.hpp:148): host copy of the packed segment
+  PackedKV packed(size_t b, size_t h) const {
+    PackedKV out;
+    out.packed_len = packed_len(b, h);
+    const size_t nb = out.packed_len / n_r();
+    for (size_t i = 0; i < nb; ++i) out.blocks.push_back(block(b, h, i));
+    return out;
+  }
+  PackedBlock block(size_t b, size_t h, size_t i) const {
+    PackedBlock blk;
+    blk.k_words.resize(info_.words_per_block);
+    blk.v_words.resize(info_.words_per_block);
+    blk.k_params.data.resize(info_.k_param_u16);
+    blk.v_params.data.resize(info_.v_param_u16);
+    const size_t g = spec_.passthrough() ? 1 : spec_.group_size;
+    if (!spec_.passthrough()) {  // quant.cpp:59-91 grids
+      if (spec_.k_axis == QuantAxis::KChannel) {
+        blk.k_params.rows = n_r() / g;
+        blk.k_params.cols = head_dim_;
+      } else {
+        blk.k_params.rows = n_r();
+        blk.k_params.cols = head_dim_ / g;
+      }
+      blk.v_params.rows = n_r();
+      blk.v_params.cols = head_dim_ / g;
+    }
+    detail::check(bdk_read_block(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h),
+                                 static_cast<uint32_t>(i), blk.k_words.data(), blk.v_words.data(),
+                                 blk.k_params.data.data(), blk.v_params.data.data()));
+    return blk;
+  }
+  // KVCache::residual_tile (kvcache.cpp:253-261): [res_len, d] fp32 each
+  void residual_tile(size_t b, size_t h, float* k_out, float* v_out) const {
+    const size_t n = res_len(b, h) * head_dim_;
+    std::vector<uint16_t> kb(n), vb(n);
+    detail::check(bdk_read_residual(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h),
+                                    kb.data(), vb.data()));
+    for (size_t i = 0; i < n; ++i) {
+      k_out[i] = f16_bits_to_f32(kb[i]);
+      v_out[i] = f16_bits_to_f32(vb[i]);
+    }
+  }
+  // KVCache::packed_tile (kvcache.cpp:263-312): device dequant, [len, d] fp32
+  void packed_tile(size_t b, size_t h, size_t t0, size_t len, float* k_out, float* v_out) const {
+    std::vector<uint16_t> kb(len * head_dim_), vb(len * head_dim_);
+    detail::check(bdk_packed_tile_host(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h),
+                                       static_cast<uint32_t>(t0), static_cast<uint32_t>(len),
+                                       kb.data(), vb.data()));
+    for (size_t i = 0; i < kb.size(); ++i) {
+      k_out[i] = f16_bits_to_f32(kb[i]);
+      v_out[i] = f16_bits_to_f32(vb[i]);
+    }
+  }
+  // KVCache::reconstruct (kvcache.cpp:314-324)
+  void reconstruct(size_t b, size_t h, std::vector<float>& k_out, std::vector<float>& v_out) const {
+    const size_t p = packed_len(b, h), r = res_len(b, h);
+    k_out.assign((p + r) * head_dim_, 0.f);
+    v_out.assign((p + r) * head_dim_, 0.f);
+    if (p) packed_tile(b, h, 0, p, k_out.data(), v_out.data());
+    if (r) residual_tile(b, h, k_out.data() + p * head_dim_, v_out.data() + p * head_dim_);
+  }
+  // KVCache::corrupt_word (kvcache.cpp:326-328)
+  void corrupt_word(size_t b, size_t h, size_t blk, size_t word, uint16_t value) {
+    detail::check(bdk_corrupt_word(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h),
+                                   static_cast<uint32_t>(blk), static_cast<uint32_t>(word),
+                                   value));
+  }
+  struct Memory {  // kvcache.hpp:165-171
+    size_t k_packed_payload_bytes = 0;
+    size_t v_packed_payload_bytes = 0;
+    size_t params_bytes = 0;
+    size_t residual_bytes = 0;
+  };
+  Memory memory() const {  // kvcache.cpp:330-345
+    uint64_t m[4];
+    detail::check(bdk_memory(h_, m));
+    return Memory{m[0], m[1], m[2], m[3]};
+  }
+  // fp16 P (false, default) or the hi/lo split PV with bit-faithful dequant
+  // (true): the reference's own 1e-5 tolerances
+  void set_precise(bool precise) { detail::check(bdk_set_precise(h_, precise ? 1 : 0)); }
+
+ private:
+  std::pair<size_t, size_t> lengths(size_t b, size_t h) const {
+    uint32_t p = 0, r = 0;
+    detail::check(bdk_cache_lengths(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h), &p,
+                                    &r));
+    return {p, r};
+  }
+  bdk_cache* h_ = nullptr;
+  size_t batch_ = 1, heads_kv_ = 1, head_dim_ = 0, warp_n_ = 1;
+  QuantSpec spec_;
+  CacheBackend backend_ = CacheBackend::Contiguous;
+  size_t page_size_ = 16;
+  bool interleave_ = true;
+  bdk_cache_info info_{};
+};
+
+// --------------------------------------------------------- attention.hpp
+struct AttnOutput {  // attention.hpp:73-84
+  size_t batch = 0;
+  size_t heads = 0;
+  size_t d = 0;
+  std::vector<float> data;
+  float* row(size_t b, size_t h) { return data.data() + (b * heads + h) * d; }
+  const float* row(size_t b, size_t h) const { return data.data() + (b * heads + h) * d; }
+};
+
+// decode_step (attention.hpp:87-88, attention.cpp:164-242)
+inline AttnOutput decode_step(KVCache& cache, const AttentionConfig& cfg, const Tensor& q,
+                              const Tensor& k_new, const Tensor& v_new) {
+  validate_config(cfg);
+  if (q.ndim() != 3 || q.dim(0) != cfg.batch || q.dim(1) != cfg.heads_q ||
+      q.dim(2) != cfg.head_dim)
+    throw ShapeError("decode_step: q must be [batch, heads_q, d]");
+  if (k_new.ndim() != 3 || k_new.dim(0) != cfg.batch || k_new.dim(1) != cfg.heads_kv ||
+      k_new.dim(2) != cfg.head_dim || v_new.ndim() != 3 || v_new.dim(0) != cfg.batch ||
+      v_new.dim(1) != cfg.heads_kv || v_new.dim(2) != cfg.head_dim)
+    throw ShapeError("decode_step: k_new / v_new must be [batch, heads_kv, d]");
+  AttnOutput out;
+  out.batch = cfg.batch;
+  out.heads = cfg.heads_q;
+  out.d = cfg.head_dim;
+  out.data.assign(cfg.batch * cfg.heads_q * cfg.head_dim, 0.f);
+  const bdk_attn_config c = detail::to_c(cfg);
+  detail::check(bdk_decode_step_host(cache.handle(), &c, q.data(), k_new.data(), v_new.data(),
+                                     out.data.data()));
+  return out;
+}
+
+}  // namespace bitkv

@@ -678,6 +678,78 @@ bdk_status bdk_decode_step_host(bdk_cache* c, const bdk_attn_config* cfg, const 
   return BDK_OK;
 }
 
+bdk_status bdk_prefill_host(bdk_cache* c, uint32_t b, uint32_t h, const uint16_t* k,
+                            const uint16_t* v, uint32_t len) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  if (len > 0 && (!k || !v)) return fail(BDK_INVALID_ARGUMENT, "null k/v");
+  const size_t n = (size_t)len * c->desc.head_dim;
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  void* d = nullptr;
+  if (n) {
+    BDK_CUDA(cudaMalloc(&d, 2 * n * 2), "cudaMalloc(prefill staging)");
+    cudaError_t e = cudaMemcpy(d, k, n * 2, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(static_cast<uint16_t*>(d) + n, v, n * 2, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(d);
+      return cuda_fail(e, "H2D prefill");
+    }
+  }
+  s = bdk_prefill(c, b, h, d, n ? static_cast<uint16_t*>(d) + n : nullptr, len, nullptr);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaFree(d);
+  if (s) return s;
+  if (e != cudaSuccess) return cuda_fail(e, "prefill");
+  return BDK_OK;
+}
+
+bdk_status bdk_append_token_host(bdk_cache* c, uint32_t b, uint32_t h, const uint16_t* k,
+                                 const uint16_t* v) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  if (!k || !v) return fail(BDK_INVALID_ARGUMENT, "null k/v row");
+  const size_t d = c->desc.head_dim;
+  s = ensure_stage(c, 4 * d + 256);
+  if (s) return s;
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  uint16_t* dk = static_cast<uint16_t*>(c->d_stage);
+  BDK_CUDA(cudaMemcpy(dk, k, d * 2, cudaMemcpyHostToDevice), "H2D row");
+  BDK_CUDA(cudaMemcpy(dk + d, v, d * 2, cudaMemcpyHostToDevice), "H2D row");
+  s = bdk_append_token(c, b, h, dk, dk + d, nullptr);
+  if (s) return s;
+  BDK_CUDA(cudaDeviceSynchronize(), "append");
+  return BDK_OK;
+}
+
+bdk_status bdk_packed_tile_host(const bdk_cache* c, uint32_t b, uint32_t h, uint32_t t0,
+                                uint32_t len, uint16_t* k_out, uint16_t* v_out) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  const int i = cell_of(c, b, h);
+  const uint32_t n_r = c->dev.G.n_r;
+  if ((uint64_t)t0 + len > (uint64_t)c->packed_blocks[i] * n_r)
+    return fail(BDK_SHAPE_ERROR, "packed_tile: range past packed segment");
+  if (len == 0) return BDK_OK;
+  if (!k_out || !v_out) return fail(BDK_INVALID_ARGUMENT, "null output");
+  const uint32_t blk0 = t0 / n_r, blk1 = (t0 + len + n_r - 1) / n_r, nb = blk1 - blk0;
+  const size_t d = c->desc.head_dim, rows = (size_t)nb * n_r;
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  uint16_t* dbuf = nullptr;
+  BDK_CUDA(cudaMalloc(&dbuf, 2 * rows * d * 2), "cudaMalloc(dequant)");
+  s = bdk_dequant_blocks(c, b, h, blk0, nb, dbuf, dbuf + rows * d, nullptr);
+  cudaError_t e = s ? cudaSuccess : cudaDeviceSynchronize();
+  const size_t off = (size_t)(t0 - blk0 * n_r) * d;
+  if (!s && e == cudaSuccess)
+    e = cudaMemcpy(k_out, dbuf + off, (size_t)len * d * 2, cudaMemcpyDeviceToHost);
+  if (!s && e == cudaSuccess)
+    e = cudaMemcpy(v_out, dbuf + rows * d + off, (size_t)len * d * 2, cudaMemcpyDeviceToHost);
+  cudaFree(dbuf);
+  if (s) return s;
+  if (e != cudaSuccess) return cuda_fail(e, "packed_tile");
+  return BDK_OK;
+}
+
 bdk_status bdk_read_block(const bdk_cache* c, uint32_t b, uint32_t h, uint32_t blk,
                           uint16_t* kw, uint16_t* vw, uint16_t* kp, uint16_t* vp) {
   bdk_status s = check_cell(c, b, h);

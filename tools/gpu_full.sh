@@ -1,0 +1,17 @@
+#!/bin/bash
+# Full measurement pass on one B200: parity tests, smoke, bench lines (all
+# workloads, both arms), ncu launch list + full capture of the hot kernel.
+mkdir -p gpurun_out/full
+O=gpurun_out/full
+python -c "from paper_2503_18773_b200 import build as B; assert not B._stale(), \"stale lib\"" || exit 3
+nvidia-smi -L > $O/gpu.txt 2>&1; lscpu > $O/host_cpu.txt 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -rA > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout 900 python bench.py > $O/bench_C2.json 2> $O/bench_C2.err
+for w in C5 C3 C1; do timeout 600 python bench.py --workload $w --no-cpu-baseline > $O/bench_$w.json 2> $O/bench_$w.err; done
+timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > $O/bench_ref_C2.json 2> $O/bench_ref_C2.err
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_C2.csv python bench.py --steps 20 --warmup 3 --soak 0 --e2e-steps 0 --no-cpu-baseline > $O/ncu_launch.log 2>&1
+for w in C2 C5 C3; do
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_fast -s 8 -c 1 -o $O/prof_$w python bench.py --workload $w --steps 5 --warmup 3 --soak 0 --e2e-steps 0 --no-cpu-baseline > $O/ncu_full_$w.log 2>&1
+done
+echo done
