@@ -25,10 +25,12 @@ def main(path):
                          text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr = rows[0]
+    units = rows[1]
     for r in rows[2:]:
         for k in KEYS:
             if k in hdr:
-                print(f"{k} = {r[hdr.index(k)]}")
+                i = hdr.index(k)
+                print(f"{k} = {r[i]} {units[i]}".rstrip())
         stalls = []
         for i, h in enumerate(hdr):
             if h.startswith('smsp__average_warps_issue_stalled_') and h.endswith('per_issue_active.ratio'):
