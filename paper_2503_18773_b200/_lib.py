@@ -52,7 +52,7 @@ SIGNATURES = {
     "bdk_append_token": (C.c_int, [vp, u32, u32, vp, vp, vp]),
     "bdk_flush_residual": (C.c_int, [vp, u32, u32, vp]),
     "bdk_decode_step": (C.c_int, [vp, C.POINTER(AttnConfig), vp, vp, vp, vp, vp]),
-    "bdk_decode_step_host": (C.c_int, [vp, C.POINTER(AttnConfig), fp, fp, fp, fp]),
+    "bdk_decode_step_host": (C.c_int, [vp, C.POINTER(AttnConfig), vp, vp, vp, vp]),
     "bdk_decode_partial": (C.c_int, [vp, C.POINTER(AttnConfig), vp, vp, vp, u32, u32, u32, vp,
                                      vp, vp]),
     "bdk_merge_partials": (C.c_int, [vp, vp, u32, u32, u32, C.c_uint64, C.c_uint64, vp, vp]),

@@ -424,10 +424,9 @@ def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None)
             validate_config(cfg)
             raise ShapeError("decode_step: q must be [batch, heads_q, d], k_new/v_new "
                              "[batch, heads_kv, d]")
-        o = np.zeros(shape_q, np.float32)
-        fpp = lambda a: a.ctypes.data_as(_L.fp)  # noqa: E731
-        _check(_L.load().bdk_decode_step_host(cache.handle(), C.byref(c), fpp(qh), fpp(kh),
-                                              fpp(vh), fpp(o)))
+        o = np.empty(shape_q, np.float32)
+        _check(_L.load().bdk_decode_step_host(cache.handle(), C.byref(c), qh.ctypes.data,
+                                              kh.ctypes.data, vh.ctypes.data, o.ctypes.data))
         return AttnOutput(cfg.batch, cfg.heads_q, cfg.head_dim, o)
     if tuple(q.shape) != shape_q or tuple(k_new.shape) != shape_kv or \
             tuple(v_new.shape) != shape_kv:

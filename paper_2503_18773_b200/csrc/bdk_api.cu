@@ -8,6 +8,7 @@
 // there is no host compute path: every numeric step runs in the sm_100a
 // kernels of bdk_kernels.cu.
 #include <cuda_runtime.h>
+#include <immintrin.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -633,15 +634,39 @@ bdk_status bdk_set_precise(bdk_cache* c, int precise) {
   return BDK_OK;
 }
 
-// host fp32 tensors -> fp16 on device (values are binary16-representable)
+// host fp32 tensors -> fp16 into the pinned staging buffer (values are
+// binary16-representable, so RNE narrowing is exact; fp16.hpp:13-70).  F16C
+// converts 8 lanes per instruction; the scalar loop covers CPUs without it
+// and the tail.
 namespace {
-__global__ void f32_to_f16_kernel(const float* in, __half* out, size_t n) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x)
-    out[i] = __float2half_rn(in[i]);
+__attribute__((target("avx,f16c"))) void f32_to_f16_f16c(const float* in, uint16_t* out,
+                                                          size_t n) {
+  size_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    const __m256 x = _mm256_loadu_ps(in + i);
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(out + i),
+                     _mm256_cvtps_ph(x, _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC));
+  }
+  for (; i < n; ++i) out[i] = static_cast<uint16_t>(_cvtss_sh(in[i], _MM_FROUND_TO_NEAREST_INT));
+}
+
+void f32_to_f16_host(const float* in, uint16_t* out, size_t n) {
+  static const bool f16c = __builtin_cpu_supports("f16c") && __builtin_cpu_supports("avx");
+  if (f16c) {
+    f32_to_f16_f16c(in, out, n);
+    return;
+  }
+  for (size_t i = 0; i < n; ++i) {
+    const __half h = __float2half_rn(in[i]);
+    std::memcpy(out + i, &h, 2);
+  }
 }
 }  // namespace
 
+// Host-tensor decode_step: the step's inputs go host fp32 -> pinned fp16
+// (F16C) -> one H2D copy; for small outputs the decode kernel writes its fp32
+// output straight into the pinned staging buffer (mapped, UVA), so the only
+// device round trip after the kernel is the stream synchronization.
 bdk_status bdk_decode_step_host(bdk_cache* c, const bdk_attn_config* cfg, const float* q,
                                 const float* k_new, const float* v_new, float* out) {
   bdk_status s = check_decode(c, cfg, true);
@@ -651,28 +676,29 @@ bdk_status bdk_decode_step_host(bdk_cache* c, const bdk_attn_config* cfg, const 
   const size_t nq = (size_t)cfg->batch * cfg->heads_q * d;
   const size_t nk = (size_t)cfg->batch * cfg->heads_kv * d;
   const size_t n_in = nq + 2 * nk;
-  // layout of the staging buffers: fp32 in [q | k | v], fp16 [q | k | v], fp32 out
-  const size_t bytes = n_in * 4 + n_in * 2 + nq * 4 + 256;
+  // staging layout (host and device alike): fp16 [q | k | v], fp32 out (128-B aligned)
+  const size_t out_off = (n_in * 2 + 127) & ~size_t(127);
+  const size_t bytes = out_off + nq * 4;
   s = ensure_stage(c, bytes);
   if (s) return s;
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
-  float* hin = static_cast<float*>(c->h_stage);
-  std::memcpy(hin, q, nq * 4);
-  std::memcpy(hin + nq, k_new, nk * 4);
-  std::memcpy(hin + nq + nk, v_new, nk * 4);
-  float* din = static_cast<float*>(c->d_stage);
-  __half* dh = reinterpret_cast<__half*>(din + n_in);
-  float* dout = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(dh + n_in) + 127) & ~uintptr_t(127));
+  uint16_t* hin = static_cast<uint16_t*>(c->h_stage);
+  f32_to_f16_host(q, hin, nq);
+  f32_to_f16_host(k_new, hin + nq, nk);
+  f32_to_f16_host(v_new, hin + nq + nk, nk);
+  __half* dh = static_cast<__half*>(c->d_stage);
+  float* hout = reinterpret_cast<float*>(static_cast<uint8_t*>(c->h_stage) + out_off);
+  // small outputs (<= 256 KiB) are stored by the kernel over PCIe into the
+  // pinned buffer (saves the D2H copy's latency); larger ones (e.g. b32 MHA,
+  // 512 KiB) go through HBM and one D2H copy, which streams faster
+  static const int zc_env = getenv("BDK_E2E_ZC") ? atoi(getenv("BDK_E2E_ZC")) : -1;
+  const bool zc = zc_env >= 0 ? zc_env != 0 : nq * 4 <= (256u << 10);
+  float* dout = zc ? hout : reinterpret_cast<float*>(static_cast<uint8_t*>(c->d_stage) + out_off);
   cudaStream_t st = 0;
-  BDK_CUDA(cudaMemcpyAsync(din, hin, n_in * 4, cudaMemcpyHostToDevice, st), "H2D");
-  f32_to_f16_kernel<<<static_cast<unsigned>(std::min<size_t>((n_in + 255) / 256, 1024)), 256, 0,
-                      st>>>(din, dh, n_in);
-  BDK_CUDA(cudaGetLastError(), "convert launch");
+  BDK_CUDA(cudaMemcpyAsync(dh, hin, n_in * 2, cudaMemcpyHostToDevice, st), "H2D");
   s = run_decode(c, cfg, dh, dh + nq, dh + nq + nk, dout, nullptr, 0, 1 << 30, st);
   if (s) return s;
-  float* hout = hin + n_in;
-  BDK_CUDA(cudaMemcpyAsync(hout, dout, nq * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  if (!zc) BDK_CUDA(cudaMemcpyAsync(hout, dout, nq * 4, cudaMemcpyDeviceToHost, st), "D2H");
   BDK_CUDA(cudaStreamSynchronize(st), "decode_step_host");
   std::memcpy(out, hout, nq * 4);
   return BDK_OK;
