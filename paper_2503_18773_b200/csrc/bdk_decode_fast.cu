@@ -51,7 +51,8 @@ constexpr int KT = D / 16;
 constexpr int QP_ROW = 272;                    // bytes per Q' head row (256 + 16 pad)
 constexpr int QP_BYTES = 8 * QP_ROW + 8 * 4;  // Q' [8 heads] + Z [8] per K group
 constexpr int OT = KT;                        // O^T accumulator tiles
-constexpr int MERGE_KC = 16;                   // contributors per merge round
+constexpr int MERGE_KC = 64;                   // contributors per merge round
+constexpr int MERGE_LB = 20;                   // slot loads in flight per thread
 
 template <int BITS, int WN, int MINB_, int GRP_>
 struct FC {
@@ -71,6 +72,13 @@ struct Smem {
   uint32_t total;
 };
 
+// column packing: with n_group <= 4 an S^T tile only fills accumulator
+// columns 0..3 (heads); the partner tile (same field shifts) is accumulated
+// into columns 4..7 of the same registers, halving the softmax work
+__host__ __device__ inline int col_pack(const Geom& G, int ng) {
+  return (ng <= 4 && (G.bits == 2 || G.bits == 4)) ? 2 : 1;
+}
+
 __host__ __device__ inline Smem smem_layout(const Geom& G, int ng, int NS, int grp) {
   Smem L;
   const int gpb = G.k_axis == 0 ? G.n_r / G.g : 1;
@@ -78,10 +86,12 @@ __host__ __device__ inline Smem smem_layout(const Geom& G, int ng, int NS, int g
   L.prep_stride = (uint32_t)((gpb * QP_BYTES + 127) / 128 * 128);
   L.prep = L.ring + NS * G.rec_bytes;
   L.merge = L.prep + NS * L.prep_stride;
-  const uint32_t merge_bytes =
-      (uint32_t)(max(G.warp_n * grp * (ng * D + 16), 24 + 2 * MERGE_KC * 8) * 4 + 64);
+  const uint32_t merge_bytes = (uint32_t)(
+      max(G.warp_n * grp * (col_pack(G, ng) * ng * D + 16), 24 + 2 * MERGE_KC * 8 + 4 * 32 * G.warp_n * grp) *
+          4 +
+      64);
   L.merge_floats = merge_bytes / 4;
-  L.total = L.merge + merge_bytes + 3 * NS * 8 + 16;
+  L.total = L.merge + merge_bytes + 3 * NS * 8 + 48;  // + flag, claim counters
   return L;
 }
 
@@ -99,6 +109,14 @@ __device__ __forceinline__ int find_cell(const int* off, int cells, long long u)
       hi = mid - 1;
   }
   return lo;
+}
+
+// next block index from a chunk position's claim counter (lane 0 claims,
+// the warp shares it)
+__device__ __forceinline__ int claim_next(int* ctr, int lane) {
+  int k = 0;
+  if (lane == 0) k = atomicAdd(ctr, 1);
+  return __shfl_sync(0xffffffffu, k, 0);
 }
 
 // online-softmax state of one consumer warp (columns = heads 2*t4, 2*t4+1)
@@ -163,8 +181,10 @@ __device__ __forceinline__ void softmax_update(float (&x)[NPAIR][4], Soft& st, f
   }
 }
 
-// consumer-warp partial of a segment -> CTA partial in `slot`
-template <int NC>
+// consumer-warp partial of a segment -> CTA partial in `slot`.  With column
+// packing (CP = 2) accumulator columns 4..7 hold a second online-softmax
+// stream of heads 0..3 (the partner tiles), merged here like another warp.
+template <int NC, int CP>
 __device__ __forceinline__ void finalize_segment(Soft st, float (&o)[OT][4], float* sm, int ng,
                                                  float* slot, float oscale) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, t4 = lane & 3;
@@ -175,49 +195,59 @@ __device__ __forceinline__ void finalize_segment(Soft st, float (&o)[OT][4], flo
     st.z0 += __shfl_xor_sync(0xffffffffu, st.z0, off);
     st.z1 += __shfl_xor_sync(0xffffffffu, st.z1, off);
   }
-  const int WS = ng * D + 16;
+  const int nvc = CP * ng;  // virtual columns: (stream, head)
+  const int WS = nvc * D + 16;
   float* so = sm + warp * WS;
-  const int h0 = 2 * t4, h1 = 2 * t4 + 1;
+  // accumulator columns 2*t4, 2*t4+1 -> (stream, head) -> virtual column
+  const int c0 = 2 * t4, c1 = 2 * t4 + 1;
+  const int hh0 = CP == 2 ? (c0 & 3) : c0, hh1 = CP == 2 ? (c1 & 3) : c1;
+  const int v0 = CP == 2 ? (c0 >> 2) * ng + hh0 : c0, v1 = CP == 2 ? (c1 >> 2) * ng + hh1 : c1;
 #pragma unroll
   for (int mt = 0; mt < KT; ++mt) {
     const int ch = mt * 16 + gid;
     // undo the subnormal-mode scale of the V codes (2^(24 - SH_REF)) and add
     // the zero-point term
-    if (h0 < ng) {
-      so[h0 * D + ch] = fmaf(o[mt][0], oscale, st.z0);
-      so[h0 * D + ch + 8] = fmaf(o[mt][2], oscale, st.z0);
+    if (hh0 < ng) {
+      so[v0 * D + ch] = fmaf(o[mt][0], oscale, st.z0);
+      so[v0 * D + ch + 8] = fmaf(o[mt][2], oscale, st.z0);
     }
-    if (h1 < ng) {
-      so[h1 * D + ch] = fmaf(o[mt][1], oscale, st.z1);
-      so[h1 * D + ch + 8] = fmaf(o[mt][3], oscale, st.z1);
+    if (hh1 < ng) {
+      so[v1 * D + ch] = fmaf(o[mt][1], oscale, st.z1);
+      so[v1 * D + ch + 8] = fmaf(o[mt][3], oscale, st.z1);
     }
   }
   if (gid == 0) {
-    if (h0 < ng) {
-      so[ng * D + h0] = st.m0;
-      so[ng * D + 8 + h0] = st.l0;
+    if (hh0 < ng) {
+      so[nvc * D + v0] = st.m0;
+      so[nvc * D + 8 + v0] = st.l0;
     }
-    if (h1 < ng) {
-      so[ng * D + h1] = st.m1;
-      so[ng * D + 8 + h1] = st.l1;
+    if (hh1 < ng) {
+      so[nvc * D + v1] = st.m1;
+      so[nvc * D + 8 + v1] = st.l1;
     }
   }
   named_bar(1, NC * 32);
   for (int i = threadIdx.x; i < ng * D; i += NC * 32) {
-    const int h = i / D;
+    const int h = i / D, ch = i % D;
     float ms = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < NC; ++w) ms = fmaxf(ms, sm[w * WS + ng * D + h]);
+    for (int w = 0; w < NC; ++w)
+#pragma unroll
+      for (int sidx = 0; sidx < CP; ++sidx) ms = fmaxf(ms, sm[w * WS + nvc * D + sidx * ng + h]);
     float acc = 0.f, l = 0.f;
 #pragma unroll
     for (int w = 0; w < NC; ++w) {
-      const float mw = sm[w * WS + ng * D + h];
-      const float f = mw == -INFINITY ? 0.f : ex2(mw - ms);
-      acc += sm[w * WS + i] * f;
-      l += sm[w * WS + ng * D + 8 + h] * f;
+#pragma unroll
+      for (int sidx = 0; sidx < CP; ++sidx) {
+        const int vc = sidx * ng + h;
+        const float mw = sm[w * WS + nvc * D + vc];
+        const float f = mw == -INFINITY ? 0.f : ex2(mw - ms);
+        acc += sm[w * WS + vc * D + ch] * f;
+        l += sm[w * WS + nvc * D + 8 + vc] * f;
+      }
     }
     slot[i] = acc;
-    if ((i % D) == 0) {
+    if (ch == 0) {
       slot[ng * D + 2 * h] = ms;
       slot[ng * D + 2 * h + 1] = l;
     }
@@ -226,26 +256,36 @@ __device__ __forceinline__ void finalize_segment(Soft st, float (&o)[OT][4], flo
 }
 
 // LSE merge of all partials of `cell` (combine, attention.cpp:142-162).
-// It runs on the kernel's tail, so it is written for latency: per chunk of
-// up to 32 contributors, (1) all (max, sum) pairs are fetched in one round
-// into shared memory and turned into per-head weights there, (2) every thread
-// owns float4s of the output and issues the chunk's loads back to back.
+// It runs on the kernel's tail, on the critical path of the step, so it is
+// written for latency: per chunk of up to MERGE_KC contributors, (1) every
+// (max, sum) pair is fetched in ONE round into shared memory, (2) each warp
+// turns the pairs of some heads into weights (lanes over contributors,
+// shuffle reductions), (3) each thread owns one float4 of the output in one
+// contributor group and issues MERGE_LB of its loads back to back.
 template <int NC>
 __device__ void merge_cell(const FastArgs& a, const Geom& G, int cell, int cta_lo, int cta_hi,
-                           float* sm) {
+                           float* sm, unsigned long long* tr) {
   constexpr int NTH = NC * 32;
   constexpr int NV = (8 * D / 4 + NTH - 1) / NTH;  // float4 outputs per thread (max)
   const int ng = a.n_group;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
   const int stride = slot_stride(ng);
+  const int st4 = stride / 4;
   const float* base = a.slots + (size_t)(cta_lo + cell) * stride;
   const int nk = cta_hi - cta_lo + 1;
   float* msh = sm;        // [8] running max per head
   float* lsh = sm + 8;    // [8] running sum per head
   float* rsh = sm + 16;   // [8] rescale of the previous chunks
   float* wk = sm + 24;    // [MERGE_KC][8] weights
-  float* lk = wk + MERGE_KC * 8;  // [MERGE_KC][8] sums
+  float* lk = wk + MERGE_KC * 8;                           // [MERGE_KC][8] sums
+  float4* red = reinterpret_cast<float4*>(lk + MERGE_KC * 8);  // [NTH] group reduction
   const int nvec = ng * D / 4;
+  // n_group <= NTH*4/D: one float4 per thread, the spare threads split the
+  // contributors into groups; else NV float4 per thread, one group
+  const bool grouped = nvec <= NTH;
+  const int ngrp = grouped ? NTH / nvec : 1;
+  const int grp = grouped ? threadIdx.x / nvec : 0;
   float4 acc[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -263,49 +303,75 @@ __device__ void merge_cell(const FastArgs& a, const Geom& G, int cell, int cta_l
       lk[k * 8 + h] = ml.y;
     }
     named_bar(1, NTH);
-    if (threadIdx.x < ng) {
-      const int h = threadIdx.x;
+    if (tr && threadIdx.x == 0 && k0 == 0) tr[14] = globaltimer();
+    for (int h = warp; h < ng; h += NC) {
+      float mx = -INFINITY;
+      for (int k = lane; k < kc; k += 32) mx = fmaxf(mx, wk[k * 8 + h]);
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
       const float mo = msh[h];
-      float mx = mo;
-      for (int k = 0; k < kc; ++k) mx = fmaxf(mx, wk[k * 8 + h]);
-      const float r = mo == -INFINITY ? 0.f : ex2(mo - mx);
-      float l = lsh[h] * r;
-      for (int k = 0; k < kc; ++k) {
+      const float mn = fmaxf(mo, mx);
+      float l = 0.f;
+      for (int k = lane; k < kc; k += 32) {
         const float m = wk[k * 8 + h];
-        const float w = m == -INFINITY ? 0.f : ex2(m - mx);
+        const float w = m == -INFINITY ? 0.f : ex2(m - mn);
         wk[k * 8 + h] = w;
         l = fmaf(lk[k * 8 + h], w, l);
       }
-      lsh[h] = l;
-      msh[h] = mx;
-      rsh[h] = r;
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+      __syncwarp();
+      if (lane == 0) {
+        const float r = mo == -INFINITY ? 0.f : ex2(mo - mn);
+        lsh[h] = fmaf(lsh[h], r, l);
+        msh[h] = mn;
+        rsh[h] = r;
+      }
     }
     named_bar(1, NTH);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const int e = threadIdx.x + v * NTH;
-      if (e < nvec) {
+      const int e = grouped ? (v == 0 ? threadIdx.x % nvec : nvec) : threadIdx.x + v * NTH;
+      if (e < nvec && grp < ngrp) {
         const int h = (4 * e) / D;
         const float r = rsh[h];
         float4 s4 = make_float4(acc[v].x * r, acc[v].y * r, acc[v].z * r, acc[v].w * r);
         const float4* po = reinterpret_cast<const float4*>(base + (size_t)k0 * stride) + e;
-        const int st4 = stride / 4;
-        float4 o[MERGE_KC];
+        for (int kb = grp; kb < kc; kb += MERGE_LB * ngrp) {
+          float4 o[MERGE_LB];
 #pragma unroll
-        for (int k = 0; k < MERGE_KC; ++k)
-          o[k] = k < kc ? __ldcg(po + (size_t)k * st4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int i = 0; i < MERGE_LB; ++i) {
+            const int k = kb + i * ngrp;
+            o[i] = k < kc ? __ldcg(po + (size_t)k * st4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
 #pragma unroll
-        for (int k = 0; k < MERGE_KC; ++k) {
-          const float w = k < kc ? wk[k * 8 + h] : 0.f;
-          s4.x = fmaf(o[k].x, w, s4.x);
-          s4.y = fmaf(o[k].y, w, s4.y);
-          s4.z = fmaf(o[k].z, w, s4.z);
-          s4.w = fmaf(o[k].w, w, s4.w);
+          for (int i = 0; i < MERGE_LB; ++i) {
+            const int k = kb + i * ngrp;
+            const float w = k < kc ? wk[k * 8 + h] : 0.f;
+            s4.x = fmaf(o[i].x, w, s4.x);
+            s4.y = fmaf(o[i].y, w, s4.y);
+            s4.z = fmaf(o[i].z, w, s4.z);
+            s4.w = fmaf(o[i].w, w, s4.w);
+          }
         }
         acc[v] = s4;
       }
     }
     named_bar(1, NTH);  // wk / lk reused by the next chunk
+    if (tr && threadIdx.x == 0 && k0 == 0) tr[15] = globaltimer();
+  }
+  if (ngrp > 1) {  // sum the contributor groups
+    red[threadIdx.x] = acc[0];
+    named_bar(1, NTH);
+    if (threadIdx.x < nvec) {
+      for (int g = 1; g < ngrp; ++g) {
+        const float4 x = red[g * nvec + threadIdx.x];
+        acc[0].x += x.x;
+        acc[0].y += x.y;
+        acc[0].z += x.z;
+        acc[0].w += x.w;
+      }
+    }
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
@@ -428,11 +494,13 @@ __device__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& p
   }
 }
 
-template <int BITS, int WN, int NS, int MINB, int GRP>
+template <int BITS, int WN, int NS, int MINB, int GRP, int CP>
 __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     decode_fast_kernel(DevCache c, FastArgs a) {
   using C = FC<BITS, WN, MINB, GRP>;
   constexpr int P = C::P, NPAIR = C::NPAIR, NC = C::NC, RB = C::RB;
+  static_assert(CP == 1 || (CP == 2 && NPAIR % 2 == 0), "column packing pairs tiles");
+  constexpr int NPK = NPAIR / CP;  // packed S^T accumulators per chunk
   static_assert(NS % GRP == 0, "stage s must always belong to consumer group s % GRP");
   // subnormal mode: the V operand P s is pre-scaled by 2^(SH_REF - sh) so the
   // accumulator holds O * 2^(SH_REF - 24) for every field shift sh
@@ -446,10 +514,11 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   uint8_t* ring = smem + L.ring;
   uint8_t* prep = smem + L.prep;
   float* merge_sm = reinterpret_cast<float*>(smem + L.merge);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.total - 3 * NS * 8 - 16);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.total - 3 * NS * 8 - 48);
   uint64_t* empty = full + NS;
   uint64_t* ready = empty + NS;
   int* flag = reinterpret_cast<int*>(ready + NS);
+  int* claim = flag + 2;  // [WN] next block per chunk position (GRP > 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, t4 = lane & 3;
   const int REC = G.rec_bytes;
 
@@ -462,6 +531,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       mbar_init(&empty[s], WN);  // the WN warps of the group that owns stage s
       mbar_init(&ready[s], 1);
     }
+    for (int i = 0; i < WN; ++i) claim[i] = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -533,7 +603,6 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   }
 
   // ------------------------------------------------------ consumer warps
-  const int grp = warp / WN;  // consumer group: takes blocks it % GRP == grp
   const int j = warp % WN;    // 16-byte chunk of every channel row
   const int tok_base = 8 * j * P;
   const int kgr = G.k_axis == 0 ? tok_base / G.g : 0;
@@ -541,6 +610,15 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   int tok_lab[2 * NPAIR];  // token offset of field position e (labels (g, e))
 #pragma unroll
   for (int e = 0; e < 2 * NPAIR; ++e) tok_lab[e] = pos_token(e, P, G.interleave);
+  // per lane: token offsets of the rows of its tile in packed accumulator i
+  // (lanes t4 >= 2 hold the partner tile i + NPAIR/2 when CP = 2)
+  int vtok[NPK][2];
+#pragma unroll
+  for (int i = 0; i < NPK; ++i) {
+    const bool partner = CP == 2 && t4 >= 2;
+    vtok[i][0] = partner ? tok_lab[2 * (i + NPAIR / 2)] : tok_lab[2 * i];
+    vtok[i][1] = partner ? tok_lab[2 * (i + NPAIR / 2) + 1] : tok_lab[2 * i + 1];
+  }
   const int stride_slot = slot_stride(ng);
 
   int it = 0;
@@ -555,17 +633,22 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
 #pragma unroll
     for (int mt = 0; mt < OT; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
 
-    // ---------------- packed blocks
-    for (long long x = u; x < pk_end; ++x, ++it) {
-      if (GRP > 1 && (it % GRP) != grp) continue;  // the other group's block
-      const int s = it % NS;
+    // ---------------- packed blocks: CTA blocks [it, it_end) of this cell.
+    // GRP > 1: the warps at chunk position j (one per group) claim blocks
+    // dynamically from a shared-memory counter, so the groups stay busy to
+    // the end of the cell whatever the warp scheduler favours
+    const int it_end = it + (int)max(0LL, pk_end - u);
+    int kn = GRP > 1 ? claim_next(claim + j, lane) : it;
+    for (int k = kn; k < it_end; k = kn) {
+      kn = GRP > 1 ? claim_next(claim + j, lane) : k + 1;  // next claim, in flight
+      const int s = k % NS;
       unsigned long long tw = 0;
       if (tr && threadIdx.x == 0) tw = globaltimer();
-      mbar_wait(&ready[s], (it / NS) & 1);
-      mbar_wait(&full[s], (it / NS) & 1);
+      mbar_wait(&ready[s], (k / NS) & 1);
+      mbar_wait(&full[s], (k / NS) & 1);
       if (tr && threadIdx.x == 0) {
         const unsigned long long now = globaltimer();
-        if (it == 0) tr[1] = now; else tr[9] += now - tw;
+        if (k == 0) tr[1] = now; else tr[9] += now - tw;
       }
       if (a.dev_flags & 1) {  // dev probe: stream only (no compute)
         __syncwarp();
@@ -576,25 +659,38 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       const uint8_t* pp = prep + (size_t)s * L.prep_stride;
       const uint8_t* qp = pp + kgr * QP_BYTES;
       const uint32_t* vpr = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes + G.kp_bytes);
-      // Q'^T B fragments (ldmatrix of the [head][channel] rows)
-      uint32_t qb[KT][2];
+      // Q'^T B fragments (ldmatrix of the [head][channel] rows; rows >= n_group
+      // are zero).  CP = 2: qh = the same heads in columns 4..7 (each lane's
+      // row address is r ^ 4, so columns 0..3 read the zero rows 4..7)
+      uint32_t qb[KT][2], qh[CP == 2 ? KT : 1][2];
       {
         const int mi = lane >> 3, r = lane & 7;
 #pragma unroll
         for (int kk = 0; kk < KT / 2; ++kk) {
           const int kt = 2 * kk + (mi >> 1);
-          const uint32_t addr = smem_u32(qp + r * QP_ROW + (kt * 16 + (mi & 1) * 8) * 2);
-          ldsm_x4(addr, qb[2 * kk][0], qb[2 * kk][1], qb[2 * kk + 1][0], qb[2 * kk + 1][1]);
+          const int cof = (kt * 16 + (mi & 1) * 8) * 2;
+          ldsm_x4(smem_u32(qp + r * QP_ROW + cof), qb[2 * kk][0], qb[2 * kk][1], qb[2 * kk + 1][0],
+                  qb[2 * kk + 1][1]);
+          if constexpr (CP == 2)
+            ldsm_x4(smem_u32(qp + (r ^ 4) * QP_ROW + cof), qh[2 * kk][0], qh[2 * kk][1],
+                    qh[2 * kk + 1][0], qh[2 * kk + 1][1]);
         }
       }
-      const float2 zz = *reinterpret_cast<const float2*>(qp + 8 * QP_ROW + 8 * t4);
+      const float2 zz =
+          *reinterpret_cast<const float2*>(qp + 8 * QP_ROW + 8 * (CP == 2 ? (t4 & 1) : t4));
       const float zs0 = zz.x * scale, zs1 = zz.y * scale;
 
-      // ---- S^T = codes_K . Q'^T over the chunk's 8*P tokens
-      float sacc[NPAIR][4];
+      // ---- S^T = codes_K . Q'^T over the chunk's 8*P tokens.  Tile pi goes
+      // to packed accumulator pi % NPK (columns 0..3 for pi < HALF, 4..7 for
+      // the partner pi >= HALF when CP = 2).  Independent HMMA chains: one per
+      // (accumulator, column half), and per channel-tile parity when few.
+      constexpr int HALF = NPAIR / 2;
+      constexpr bool KSPLIT = NPAIR <= 2;
+      constexpr int NCH = NPK * CP * (KSPLIT ? 2 : 1);
+      float chn[NCH][4];
 #pragma unroll
-      for (int i = 0; i < NPAIR; ++i) sacc[i][0] = sacc[i][1] = sacc[i][2] = sacc[i][3] = 0.f;
-      {
+      for (int i = 0; i < NCH; ++i) chn[i][0] = chn[i][1] = chn[i][2] = chn[i][3] = 0.f;
+      if (!(a.dev_flags & 4)) {  // dev probe 4: skip the K side
         const uint32_t kw = smem_u32(rec);
         uint32_t kr[4][4];
 #pragma unroll
@@ -622,15 +718,30 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
             BDK_KEXT(2)
             BDK_KEXT(3)
 #undef BDK_KEXT
-            mma16816(sacc[pi], af, qb[kt][0], qb[kt][1]);
+            const int f = (CP == 2 && pi >= HALF) ? 1 : 0;
+            const int ci = pi % NPK + NPK * (f + CP * (KSPLIT ? (kt & 1) : 0));
+            if (f)
+              mma16816(chn[ci], af, qh[CP == 2 ? kt : 0][0], qh[CP == 2 ? kt : 0][1]);
+            else
+              mma16816(chn[ci], af, qb[kt][0], qb[kt][1]);
           }
         }
       }
-      // ---- logits (log2 domain), online softmax
-      // S = S' 2^(24 - sh) + Z (rows gid / gid+8 hold fields 2i / 2i+1), in
-      // the log2 domain of the softmax
+      float sacc[NPK][4];
 #pragma unroll
-      for (int i = 0; i < NPAIR; ++i) {
+      for (int i = 0; i < NPK; ++i)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          float x = chn[i][r];
+#pragma unroll
+          for (int k = 1; k < NCH / NPK; ++k) x += chn[i + k * NPK][r];
+          sacc[i][r] = x;
+        }
+      // ---- logits (log2 domain), online softmax
+      // S = S' 2^(24 - sh) + Z (rows gid / gid+8 hold fields 2i / 2i+1; the
+      // partner tile i + HALF has the same field shifts), in the log2 domain
+#pragma unroll
+      for (int i = 0; i < NPK; ++i) {
         const float al = scale * (float)(1 << (24 - ((2 * i) % P) * BITS % 8));
         const float ah = scale * (float)(1 << (24 - ((2 * i + 1) % P) * BITS % 8));
         sacc[i][0] = fmaf(sacc[i][0], al, zs0);
@@ -638,16 +749,17 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
         sacc[i][2] = fmaf(sacc[i][2], ah, zs0);
         sacc[i][3] = fmaf(sacc[i][3], ah, zs1);
       }
-      softmax_update<NPAIR>(sacc, st, o);
+      softmax_update<NPK>(sacc, st, o);
       // ---- P' = P * s_t (V token scale folded), zero term, P'^T fragments
-      uint32_t pb[NPAIR][2];
+      uint32_t pb[NPK][2];
 #pragma unroll
-      for (int i = 0; i < NPAIR; ++i) {
-        // V (scale, zero) of the tokens of rows gid / gid+8 (fields 2i / 2i+1);
-        // the scale carries 2^(SH_REF - sh) of the field's subnormal shift
+      for (int i = 0; i < NPK; ++i) {
+        // V (scale, zero) of the tokens of rows gid / gid+8 (fields 2i / 2i+1
+        // of this lane's tile); the scale carries 2^(SH_REF - sh) of the
+        // field's subnormal shift
         const int g0 = (8 * j + gid) * P;
-        const float2 pa = __half22float2(u2h(vpr[g0 + tok_lab[2 * i]]));
-        const float2 pz = __half22float2(u2h(vpr[g0 + tok_lab[2 * i + 1]]));
+        const float2 pa = __half22float2(u2h(vpr[g0 + vtok[i][0]]));
+        const float2 pz = __half22float2(u2h(vpr[g0 + vtok[i][1]]));
         const float2 sz0 = make_float2(
             pa.x * (float)(1 << (SH_REF + 8)) / (float)(1 << (8 + ((2 * i) % P) * BITS % 8)), pa.y);
         const float2 sz1 = make_float2(
@@ -657,6 +769,18 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
         st.z1 = fmaf(sacc[i][1], sz0.y, fmaf(sacc[i][3], sz1.y, st.z1));
         pb[i][0] = movmatrix_t(pack_h2(sacc[i][0] * sz0.x, sacc[i][1] * sz0.x));
         pb[i][1] = movmatrix_t(pack_h2(sacc[i][2] * sz1.x, sacc[i][3] * sz1.x));
+      }
+      // CP = 2: P'^T of tile i keeps only its column half (head columns n =
+      // gid after the transpose)
+      uint32_t pbh[CP == 2 ? NPK : 1][2];
+      if constexpr (CP == 2) {
+#pragma unroll
+        for (int i = 0; i < NPK; ++i) {
+          pbh[i][0] = gid >= 4 ? pb[i][0] : 0u;
+          pbh[i][1] = gid >= 4 ? pb[i][1] : 0u;
+          pb[i][0] = gid < 4 ? pb[i][0] : 0u;
+          pb[i][1] = gid < 4 ? pb[i][1] : 0u;
+        }
       }
       // ---- O^T += codes_V^T . P'^T
       {
@@ -672,6 +796,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
         if (lane == 0) mbar_arrive(&empty[s]);  // ring slot + prep slot are free
 #pragma unroll
         for (int mt = 0; mt < KT; ++mt) {
+          if (a.dev_flags & 8) break;  // dev probe 8: skip the V side
           const uint32_t ra = vr[mt / 2][2 * (mt % 2)], rb = vr[mt / 2][2 * (mt % 2) + 1];
           const uint32_t ra8 = ra >> 8, rb8 = rb >> 8;
 #pragma unroll
@@ -689,12 +814,16 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
             BDK_VEXT(2)
             BDK_VEXT(3)
 #undef BDK_VEXT
-            mma16816(o[mt], af, pb[pi][0], pb[pi][1]);
+            if (CP == 2 && pi >= HALF)
+              mma16816(o[mt], af, pbh[CP == 2 ? pi - HALF : 0][0], pbh[CP == 2 ? pi - HALF : 0][1]);
+            else
+              mma16816(o[mt], af, pb[pi % NPK][0], pb[pi % NPK][1]);
           }
         }
       }
     }
 
+    it = it_end;
     if (tr && threadIdx.x == 0) tr[2] = globaltimer();
     // ---------------- residual window (fp16), append fused.  Residual unit r
     // of a cell covers tokens [r*RT, (r+1)*RT) (RT = 16 per consumer warp);
@@ -767,10 +896,13 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
         }
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt) mma16816(sacc[0], ka[kt], qb[kt][0], qb[kt][1]);
-        sacc[0][0] = v0 ? sacc[0][0] * scale : -INFINITY;
-        sacc[0][1] = v0 ? sacc[0][1] * scale : -INFINITY;
-        sacc[0][2] = v1 ? sacc[0][2] * scale : -INFINITY;
-        sacc[0][3] = v1 ? sacc[0][3] * scale : -INFINITY;
+        // CP = 2: columns 4..7 are the partner stream, which the residual
+        // tokens do not feed
+        const bool live = CP == 1 || t4 < 2;
+        sacc[0][0] = v0 && live ? sacc[0][0] * scale : -INFINITY;
+        sacc[0][1] = v0 && live ? sacc[0][1] * scale : -INFINITY;
+        sacc[0][2] = v1 && live ? sacc[0][2] * scale : -INFINITY;
+        sacc[0][3] = v1 && live ? sacc[0][3] * scale : -INFINITY;
         softmax_update<1>(sacc, st, o);
         const uint32_t pb0 = movmatrix_t(pack_h2(sacc[0][0], sacc[0][1]));
         const uint32_t pb1 = movmatrix_t(pack_h2(sacc[0][2], sacc[0][3]));
@@ -789,7 +921,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     // ---------------- segment partial -> slot (CTA + cell), completion count
     if (tr && threadIdx.x == 0) tr[3] = globaltimer();
     float* slot = a.slots + (size_t)(blockIdx.x + cell) * stride_slot;
-    finalize_segment<NC>(st, o, merge_sm, ng, slot, oscale_seg);  // ends with a barrier
+    finalize_segment<NC, CP>(st, o, merge_sm, ng, slot, oscale_seg);  // ends with a barrier
     if (tr && threadIdx.x == 0) tr[4] = globaltimer();
     const int lo = cta_of_unit(cb, T, N), hi = cta_of_unit(ce - 1, T, N);
     if (threadIdx.x == 0) {
@@ -805,7 +937,8 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       *flag = last;
     }
     named_bar(1, NC * 32);
-    if (*flag) merge_cell<NC>(a, G, cell, lo, hi, merge_sm);
+    if (tr && threadIdx.x == 0) tr[10] = globaltimer();
+    if (*flag) merge_cell<NC>(a, G, cell, lo, hi, merge_sm, tr);
     if (tr && threadIdx.x == 0) {
       tr[5] = globaltimer();
       tr[6] = (unsigned long long)(*flag);
@@ -814,6 +947,9 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       tr[8] = smid;
     }
+    // every consumer warp has left its claim loop: restart the claims at the
+    // next cell's first block
+    if (GRP > 1 && threadIdx.x < WN) claim[threadIdx.x] = it;
     named_bar(1, NC * 32);  // flag / merge smem reuse by the next segment
     u = seg_end;
   }
@@ -841,8 +977,13 @@ struct Variant {
 };
 
 template <int BITS, int WN, int NS, int MINB, int GRP>
-static Variant variant() {
-  return Variant{reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP>), NS,
+static Variant variant(int cp) {
+  if constexpr (BITS != 8) {
+    if (cp == 2)
+      return Variant{reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP, 2>),
+                     NS, GRP};
+  }
+  return Variant{reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP, 1>), NS,
                  GRP};
 }
 
@@ -857,10 +998,12 @@ static int variant_knob() {
 // default: two co-resident CTAs per SM, one consumer group each, 4-stage ring
 // (measured best on B200); knob 2 = one CTA per SM with two consumer groups
 // over an 8-stage ring (balanced finish, lower throughput), 3 = three groups.
-static Variant fast_kernel(const Geom& G) {
+static Variant fast_kernel(const Geom& G, int ng) {
   const int v = variant_knob();
+  static const bool cp_off = getenv("BDK_COLPACK") && atoi(getenv("BDK_COLPACK")) == 0;
+  const int cp = cp_off ? 1 : col_pack(G, ng);
 #define BDK_SEL(B, W, NS, MB, GR) \
-  if (G.bits == B && G.warp_n == W) return variant<B, W, NS, MB, GR>();
+  if (G.bits == B && G.warp_n == W) return variant<B, W, NS, MB, GR>(cp);
   if (v == 2) {
     BDK_SEL(2, 4, 8, 1, 2) BDK_SEL(4, 4, 8, 1, 2)
   } else if (v == 3) {
@@ -875,10 +1018,10 @@ static Variant fast_kernel(const Geom& G) {
 
 static int fast_threads(const Geom& G, int grp) { return (G.warp_n * grp + 1 + grp) * 32; }
 
-int fast_residual_tokens(const Geom& G) { return 16 * G.warp_n * fast_kernel(G).grp; }
+int fast_residual_tokens(const Geom& G) { return 16 * G.warp_n * fast_kernel(G, 1).grp; }
 
 int fast_decode_ctas_per_sm(const Geom& G, int n_group) {
-  const Variant k = fast_kernel(G);
+  const Variant k = fast_kernel(G, n_group);
   if (!k.fn) return 0;
   const Smem L = smem_layout(G, n_group, k.ns, k.grp);
   if (cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) !=
@@ -892,7 +1035,7 @@ int fast_decode_ctas_per_sm(const Geom& G, int n_group) {
 }
 
 cudaError_t launch_decode_fast(const DevCache& c, const FastArgs& a, cudaStream_t s) {
-  const Variant k = fast_kernel(c.G);
+  const Variant k = fast_kernel(c.G, a.n_group);
   if (!k.fn) return cudaErrorInvalidValue;
   const Smem L = smem_layout(c.G, a.n_group, k.ns, k.grp);
   DevCache cc = c;
