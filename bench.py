@@ -1,6 +1,6 @@
 """bench.py -- BitDecoding decode hot path on B200: quantized-KV decode attention.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2|C5|C3|C1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2|C5|C3|C1|C4|C4b2]
                     [--impl ours|reference] [--no-cpu-baseline] [--extra]
 
 Prints ONE JSON line (rank 0).  The metric is BASELINE.json's: decode-attention
@@ -51,7 +51,14 @@ WORKLOADS = {
                desc="LLaMA-2-7B MHA decode attn, b32, 32q/32kv, d128, 4-bit g128 N_r128, 8K"),
     "C5": dict(batch=1, hq=32, hkv=8, bits=4, warp_n=4, g=128, seq=131072,
                desc="LLaMA-3.1-8B decode attn, b1, 32q/8kv, d128, 4-bit g128 N_r128, 128K"),
+    # quantize-and-pack throughput (BASELINE configs[3]): prefill of 32K fp16
+    # K/V tokens x 8 KV heads into the 4-bit / 2-bit layouts
+    "C4": dict(batch=1, hq=32, hkv=8, bits=4, warp_n=4, g=128, seq=32768, qpack=True,
+               desc="qpack: 32K fp16 K/V tokens x 8 KV heads, d128 -> 4-bit g128 N_r128"),
+    "C4b2": dict(batch=1, hq=32, hkv=8, bits=2, warp_n=4, g=128, seq=32768, qpack=True,
+                 desc="qpack: 32K fp16 K/V tokens x 8 KV heads, d128 -> 2-bit g128 N_r256"),
 }
+QPACK_METRIC = "quantize-and-pack throughput (GB/s of fp16 read + packed written), C4"
 METRIC = ("decode-attn latency (µs) & HBM GB/s on quantized KV vs 8 TB/s, 4/2-bit, "
           "32K–128K")
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
@@ -365,6 +372,149 @@ def load_traffic(workload):
         return None
 
 
+# ------------------------------------------------ C4: quantize-and-pack
+def qpack_bytes(w):
+    """fp16 K/V read + packed words and (scale, zero) params written
+    (SURVEY.md 8(d), C4 rows)."""
+    n_r = 8 * w["warp_n"] * (16 // w["bits"])
+    cells = w["batch"] * w["hkv"]
+    plen = w["seq"] - w["seq"] % n_r
+    rd = 2 * cells * w["seq"] * D * 2
+    wr = cells * (2 * plen * D * w["bits"] // 8 + 4 * D * plen // w["g"] + 4 * plen * D // w["g"])
+    return rd, wr
+
+
+def run_qpack(args, w, world, rank, local):
+    """Prefill (KVCache::prefill, kvcache.cpp:155-168) of every cell: one
+    fused quantize+pack launch per step into a fresh cache."""
+    import torch
+    import torch.distributed as dist
+    from paper_2503_18773_b200 import bitkv as bk
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    spec = bk.QuantSpec(w["bits"], bk.QuantAxis.KChannel, w["g"])
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4321 + rank)
+    shape = (w["batch"], w["hkv"], w["seq"], D)
+    k = torch.randn(shape, generator=gen, device=dev, dtype=torch.float16)
+    v = torch.randn(shape, generator=gen, device=dev, dtype=torch.float16)
+    K, W = args.steps, args.warmup
+    n_c = min(K, 32)
+    caches = [bk.KVCache(w["batch"], w["hkv"], D, w["warp_n"], spec, max_tokens=w["seq"],
+                         device=local) for _ in range(n_c)]
+    for i in range(W):
+        caches[i % n_c].reset()
+        caches[i % n_c].prefill_all(k, v)
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    ms, done = 0.0, 0
+    n_launch0 = sum(c.launch_count() for c in caches)
+    while done < K:
+        n = min(n_c, K - done)
+        for c in caches[:n]:
+            c.reset()  # untimed: the timed region is the prefill launches only
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for c in caches[:n]:
+            c.prefill_all(k, v)
+        e1.record()
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+        done += n
+    clk = clocks.stop()
+    n_launched = sum(c.launch_count() for c in caches) - n_launch0
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    rd, wr = qpack_bytes(w)
+    mem = caches[0].memory().__dict__
+    wr_live = mem["k_packed_payload_bytes"] + mem["v_packed_payload_bytes"] + mem["params_bytes"]
+    assert wr_live == wr, (wr_live, wr)
+    # e2e: host (pinned) fp16 K/V -> KVCache.prefill_all through the public
+    # API: H2D copy of the step's K/V + the qpack launch, synchronized
+    kh = k.cpu().pin_memory()
+    vh = v.cpu().pin_memory()
+    kd, vd = torch.empty_like(k), torch.empty_like(v)
+    e2e_steps = max(1, min(5, args.e2e_steps))
+    e2e_s = 0.0
+    for _ in range(e2e_steps):
+        c = caches[0]
+        c.reset()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        kd.copy_(kh, non_blocking=True)
+        vd.copy_(vh, non_blocking=True)
+        c.prefill_all(kd, vd)
+        torch.cuda.synchronize()
+        e2e_s += time.perf_counter() - t0
+    if rank != 0:
+        return None
+    per_step = (rd + wr)
+    gbs = per_step * world * K / (ms * 1e-3) / 1e9
+    achieved = per_step / (ms / K * 1e-3) / 1e9
+    peak, peak_src = peak_hbm()
+    res = {
+        "metric": QPACK_METRIC, "value": round(gbs, 1), "unit": "GB/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(ms / K, 5),
+        "latency_us": round(ms / K * 1e3, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": f"fp16 -> u{w['bits']} codes (bit-exact integer pack)",
+        "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {w['desc']}", "cells": w["batch"] * w["hkv"],
+                   "seq_len": w["seq"], "bits": w["bits"], "group_size": w["g"],
+                   "warp_n": w["warp_n"], "parallelism": "single GPU" if world == 1
+                   else f"dp{world} (independent caches)",
+                   "l2": "inputs 2 x %.0f MB fp16 (> L2), fresh cache per step" % (rd / 2e6),
+                   "bytes_read_per_step": rd, "bytes_written_per_step": wr},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "peak_source": peak_src,
+                     "kernel": "bdk::prefill_kernel (fused quantize + pack, bdk_qpack.cuh)",
+                     "duration": "timed region / prefill launches (events, one launch per step)",
+                     "algorithmic_bytes_per_launch": per_step,
+                     "traffic": load_traffic(args.workload)},
+        "e2e": {"value": round(per_step * e2e_steps / e2e_s / 1e9, 2), "unit": "GB/s",
+                "latency_us": round(e2e_s / e2e_steps * 1e6, 1),
+                "h2d_bytes_per_step": rd, "d2h_bytes_per_step": 0,
+                "path": "pinned host fp16 K/V -> H2D -> KVCache.prefill_all (qpack) -> sync",
+                "clock": "host perf_counter"},
+        "gpu_launches": n_launched, "clocks": clk, "cpu_baseline": None,
+    }
+    return res
+
+
+def cpu_qpack_reference(w):
+    """The reference's prefill (single-threaded by construction, bench.cpp:
+    132-139) through its own run_bench: (GB/s, seconds, kind, sample)."""
+    from oracle import oracle as O
+    rd, wr = qpack_bytes(w)
+    if O.have_ref():
+        r = O.ref_run_bench(mode=0, seq_len=w["seq"], batch=w["batch"], heads_q=w["hq"],
+                            heads_kv=w["hkv"], head_dim=D, bits=w["bits"], group_size=w["g"],
+                            k_axis=0, num_splits=4, steps=1, seed=0, tile_n=64,
+                            warp_n=w["warp_n"])
+        sec = r["prefill_seconds"]
+        return ((rd + wr) / sec / 1e9, sec, "reference",
+                f"reference run_bench prefill_seconds (bench.cpp:132-139), full C4 shape, "
+                f"1 thread by construction")
+    import numpy as np
+    g = O.Gauss(0)
+    oc = O.OracleCache(w["batch"], w["hkv"], D, w["warp_n"], w["bits"], 0, w["g"], True,
+                       max_tokens=w["seq"])
+    ks = [g.rounded(w["seq"] * D).reshape(w["seq"], D) for _ in range(2 * w["hkv"])]
+    t0 = time.perf_counter()
+    for h in range(w["hkv"]):
+        oc.prefill(0, h, ks[2 * h], ks[2 * h + 1])
+    sec = time.perf_counter() - t0
+    del np
+    return ((rd + wr) / sec / 1e9, sec, "port",
+            "oracle C restatement prefill, full C4 shape, 1 thread")
+
+
 # ------------------------------------------------------- CPU reference arm
 def cpu_reference(w, steps, warm=1):
     """The unmodified reference engine (oracle/_ref) via its own run_bench,
@@ -417,6 +567,18 @@ def cpu_reference(w, steps, warm=1):
 def run_reference_arm(args, w, world, rank):
     if rank != 0:
         return None
+    if w.get("qpack"):
+        gbs, sec, kind, sample = cpu_qpack_reference(w)
+        return {"impl": "reference", "metric": QPACK_METRIC, "value": round(gbs, 4),
+                "unit": "GB/s", "n_gpus": world, "steps": 1, "warmup": 0,
+                "ms_per_step": round(sec * 1e3, 3), "latency_us": round(sec * 1e6, 1),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": f"fp32 -> u{w['bits']} codes (CPU)", "data": "synthetic",
+                "config": {"workload": f"{args.workload}: {w['desc']}", "seq_len": w["seq"]},
+                "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1,
+                                 "kind": kind, "sample": sample},
+                "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
     steps = args.steps
     # bound the run: the reference step at C2/C5 is ~1 s on 8 cores
     est = {"C1": 0.05, "C2": 1.7, "C3": 5.0, "C5": 0.9}[args.workload] * 8 / (os.cpu_count() or 8)
@@ -465,6 +627,16 @@ def main():
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
+        if w.get("qpack"):
+            res = run_qpack(args, w, world, rank, local)
+            if res is not None and world == 1 and not args.no_cpu_baseline:
+                gbs, sec, kind, sample = cpu_qpack_reference(w)
+                res["cpu_baseline"] = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1,
+                                       "kind": kind, "sample": sample,
+                                       "ms_per_step": round(sec * 1e3, 2)}
+            if res is not None:
+                print(json.dumps(res), flush=True)
+            return
         res = run_ours(args, w, world, rank, local)
         if res is not None:
             if world == 1 and not args.no_cpu_baseline:

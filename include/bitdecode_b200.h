@@ -107,6 +107,11 @@ BDK_API bdk_status bdk_cache_get_info(const bdk_cache* cache, bdk_cache_info* in
 BDK_API bdk_status bdk_cache_lengths(const bdk_cache* cache, uint32_t b, uint32_t h,
                                      uint32_t* packed_len, uint32_t* res_len);
 
+/* Empty every cell (packed_len = res_len = 0), stream-ordered; the arena is
+ * kept.  Equivalent to constructing a fresh KVCache of the same geometry
+ * (kvcache.cpp:114-148) without reallocating device memory. */
+BDK_API bdk_status bdk_cache_reset(bdk_cache* cache, void* stream);
+
 /* ------------------------------------------------- cache state machine */
 /* KVCache::prefill (kvcache.cpp:155-168): fused quantize+pack of the first
  * len - len % N_r tokens (bit-exact), tail into the residual.

@@ -46,6 +46,7 @@ SIGNATURES = {
     "bdk_cache_lengths": (C.c_int, [vp, u32, u32, C.POINTER(u32), C.POINTER(u32)]),
     "bdk_prefill": (C.c_int, [vp, u32, u32, vp, vp, u32, vp]),
     "bdk_prefill_all": (C.c_int, [vp, vp, vp, u32, vp]),
+    "bdk_cache_reset": (C.c_int, [vp, vp]),
     "bdk_prefill_host": (C.c_int, [vp, u32, u32, u16p, u16p, u32]),
     "bdk_append_token_host": (C.c_int, [vp, u32, u32, u16p, u16p]),
     "bdk_packed_tile_host": (C.c_int, [vp, u32, u32, u32, u32, u16p, u16p]),

@@ -279,6 +279,11 @@ class KVCache:
                                          C.c_void_p(v.data_ptr()), k.shape[-2], _stream_ptr()))
         self._keep = (k, v)
 
+    def reset(self) -> None:
+        """Empty every cell (a fresh KVCache of the same geometry, kvcache.cpp:114-148),
+        keeping the device arena; stream-ordered."""
+        _check(_L.load().bdk_cache_reset(self._h, _stream_ptr()))
+
     def append_token(self, b: int, h: int, k_row, v_row) -> None:
         """KVCache::append_token (kvcache.cpp:170-182)."""
         k = _as_f16_cuda(k_row, (self._d,), self._device)

@@ -532,6 +532,20 @@ bdk_status bdk_prefill(bdk_cache* c, uint32_t b, uint32_t h, const void* k, cons
   return BDK_OK;
 }
 
+bdk_status bdk_cache_reset(bdk_cache* c, void* stream) {
+  if (!c) return fail(BDK_INVALID_ARGUMENT, "null cache");
+  const size_t cells = c->res_len.size();
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(cudaMemsetAsync(c->dev.packed_blocks, 0, cells * sizeof(int), as_stream(stream)),
+           "reset packed_blocks");
+  BDK_CUDA(cudaMemsetAsync(c->dev.res_len, 0, cells * sizeof(int), as_stream(stream)),
+           "reset res_len");
+  std::fill(c->packed_blocks.begin(), c->packed_blocks.end(), 0);
+  std::fill(c->res_len.begin(), c->res_len.end(), 0);
+  c->blocks_written = true;
+  return BDK_OK;
+}
+
 bdk_status bdk_prefill_all(bdk_cache* c, const void* k, const void* v, uint32_t len,
                            void* stream) {
   if (!c) return fail(BDK_INVALID_ARGUMENT, "null cache");

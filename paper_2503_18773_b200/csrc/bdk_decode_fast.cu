@@ -263,7 +263,7 @@ __device__ __forceinline__ void finalize_segment(Soft st, float (&o)[OT][4], flo
 // shuffle reductions), (3) each thread owns one float4 of the output in one
 // contributor group and issues MERGE_LB of its loads back to back.
 template <int NC>
-__device__ void merge_cell(const FastArgs& a, const Geom& G, int cell, int cta_lo, int cta_hi,
+__device__ void merge_cell(const FastArgs& a, const Geom& G, int cell, const float* base, int nk,
                            float* sm, unsigned long long* tr) {
   constexpr int NTH = NC * 32;
   constexpr int NV = (8 * D / 4 + NTH - 1) / NTH;  // float4 outputs per thread (max)
@@ -272,8 +272,7 @@ __device__ void merge_cell(const FastArgs& a, const Geom& G, int cell, int cta_l
   const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
   const int stride = slot_stride(ng);
   const int st4 = stride / 4;
-  const float* base = a.slots + (size_t)(cta_lo + cell) * stride;
-  const int nk = cta_hi - cta_lo + 1;
+  (void)cell;
   float* msh = sm;        // [8] running max per head
   float* lsh = sm + 8;    // [8] running sum per head
   float* rsh = sm + 16;   // [8] rescale of the previous chunks
@@ -390,6 +389,53 @@ __device__ void merge_cell(const FastArgs& a, const Geom& G, int cell, int cta_l
   }
 }
 
+// Fold of one staged block for the prep warp: Q'[h][c] = fp16(q[h][c] s_c)
+// and Z[h] = sum_c q[h][c] z_c for every K group of the block (q2 / qf: this
+// lane's query channels as half2 / fp32).
+template <int NH>
+__device__ __forceinline__ void prep_fold(const uint8_t* rec, uint8_t* pp, const Geom& G, int ng,
+                                          const uint32_t (&q2)[D / (32 / NH) / 2],
+                                          const float (&qf)[D / (32 / NH)]) {
+  constexpr int LPH = 32 / NH;  // lanes per head
+  constexpr int CPL = D / LPH;  // channels per lane
+  constexpr int H2 = CPL / 2;   // half2 per lane
+  const int lane = threadIdx.x & 31;
+  const int h = lane % NH, cbk = lane / NH;
+  const int gpb = G.k_axis == 0 ? G.n_r / G.g : 1;
+  const uint32_t* kp = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes);
+  for (int gr = 0; gr < gpb; ++gr) {
+    uint8_t* qp = pp + gr * QP_BYTES;
+    float za = 0.f, zb = 0.f;
+    uint32_t qo[H2];
+#pragma unroll
+    for (int i = 0; i < H2; ++i) {
+      const uint2 pr = *reinterpret_cast<const uint2*>(kp + gr * D + cbk * CPL + 2 * i);
+      const __half2 s2 = u2h(prmt(pr.x, pr.y, 0x5410));
+      const __half2 z2 = u2h(prmt(pr.x, pr.y, 0x7632));
+      qo[i] = h2u(__hmul2(u2h(q2[i]), s2));
+      const float2 zf = __half22float2(z2);
+      za = fmaf(qf[2 * i], zf.x, za);
+      zb = fmaf(qf[2 * i + 1], zf.y, zb);
+    }
+    if (h < ng) {
+      uint32_t* dst = reinterpret_cast<uint32_t*>(qp + h * QP_ROW + cbk * CPL * 2);
+      if constexpr (H2 % 4 == 0) {
+#pragma unroll
+        for (int v = 0; v < H2 / 4; ++v)
+          reinterpret_cast<uint4*>(dst)[v] =
+              make_uint4(qo[4 * v], qo[4 * v + 1], qo[4 * v + 2], qo[4 * v + 3]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < H2; ++v) dst[v] = qo[v];
+      }
+    }
+    float zacc = za + zb;
+#pragma unroll
+    for (int off = NH; off < 32; off <<= 1) zacc += __shfl_xor_sync(0xffffffffu, zacc, off);
+    if (cbk == 0 && h < ng) reinterpret_cast<float*>(qp + 8 * QP_ROW)[h] = zacc;
+  }
+}
+
 struct PrepCtx {
   const uint8_t* ring;
   uint8_t* prep;
@@ -450,40 +496,8 @@ __device__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& p
         const unsigned long long tb = (px.tr && lane == 0) ? globaltimer() : 0ull;
         if (px.tr && lane == 0) px.tr[12] += tb - tw;
         if (!(a.dev_flags & 2)) {
-          const uint8_t* rec = px.ring + (size_t)s * px.rec;
-          uint8_t* pp = px.prep + (size_t)s * px.prep_stride;
-          const uint32_t* kp = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes);
-          for (int gr = 0; gr < gpb; ++gr) {
-            uint8_t* qp = pp + gr * QP_BYTES;
-            float za = 0.f, zb = 0.f;
-            uint32_t qo[H2];
-#pragma unroll
-            for (int i = 0; i < H2; ++i) {
-              const uint2 pr = *reinterpret_cast<const uint2*>(kp + gr * D + cbk * CPL + 2 * i);
-              const __half2 s2 = u2h(prmt(pr.x, pr.y, 0x5410));
-              const __half2 z2 = u2h(prmt(pr.x, pr.y, 0x7632));
-              qo[i] = h2u(__hmul2(u2h(q2[i]), s2));
-              const float2 zf = __half22float2(z2);
-              za = fmaf(qf[2 * i], zf.x, za);
-              zb = fmaf(qf[2 * i + 1], zf.y, zb);
-            }
-            if (h < ng) {
-              uint32_t* dst = reinterpret_cast<uint32_t*>(qp + h * QP_ROW + cbk * CPL * 2);
-              if constexpr (H2 % 4 == 0) {
-#pragma unroll
-                for (int v = 0; v < H2 / 4; ++v)
-                  reinterpret_cast<uint4*>(dst)[v] =
-                      make_uint4(qo[4 * v], qo[4 * v + 1], qo[4 * v + 2], qo[4 * v + 3]);
-              } else {
-#pragma unroll
-                for (int v = 0; v < H2; ++v) dst[v] = qo[v];
-              }
-            }
-            float zacc = za + zb;
-#pragma unroll
-            for (int off = NH; off < 32; off <<= 1) zacc += __shfl_xor_sync(0xffffffffu, zacc, off);
-            if (cbk == 0 && h < ng) reinterpret_cast<float*>(qp + 8 * QP_ROW)[h] = zacc;
-          }
+          prep_fold<NH>(px.ring + (size_t)s * px.rec, px.prep + (size_t)s * px.prep_stride, G, ng, q2,
+                        qf);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&px.ready[s]);
@@ -491,6 +505,266 @@ __device__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& p
       }
     }
     u = seg_end;
+  }
+}
+
+// One packed block (one 16-byte chunk j of every channel row) of a consumer
+// warp: S^T = codes_K . Q'^T, online softmax, O^T += codes_V^T . P'^T.
+// `rec` is the staged block record, `qp` its folded query (prep warp).
+template <int BITS, int WN, int CP>
+__device__ __forceinline__ void consume_block(const uint8_t* rec, const uint8_t* qp, const Geom& G,
+                                              int j, float scale,
+                                              const int (&vtok)[FC<BITS, WN, 1, 1>::NPAIR / CP][2],
+                                              Soft& st, float (&o)[OT][4], uint64_t* empty_s,
+                                              int dev_flags) {
+  using C = FC<BITS, WN, 1, 1>;
+  constexpr int P = C::P, NPAIR = C::NPAIR, RB = C::RB;
+  constexpr int NPK = NPAIR / CP;
+  constexpr int SH_REF = BITS == 8 ? 0 : 2;
+  const int lane = threadIdx.x & 31, gid = lane >> 2, t4 = lane & 3;
+      const uint32_t* vpr = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes + G.kp_bytes);
+  // Q'^T B fragments (ldmatrix of the [head][channel] rows; rows >= n_group
+  // are zero).  CP = 2: qh = the same heads in columns 4..7 (each lane's
+  // row address is r ^ 4, so columns 0..3 read the zero rows 4..7)
+  uint32_t qb[KT][2], qh[CP == 2 ? KT : 1][2];
+  {
+    const int mi = lane >> 3, r = lane & 7;
+#pragma unroll
+    for (int kk = 0; kk < KT / 2; ++kk) {
+      const int kt = 2 * kk + (mi >> 1);
+      const int cof = (kt * 16 + (mi & 1) * 8) * 2;
+      ldsm_x4(smem_u32(qp + r * QP_ROW + cof), qb[2 * kk][0], qb[2 * kk][1], qb[2 * kk + 1][0],
+              qb[2 * kk + 1][1]);
+      if constexpr (CP == 2)
+        ldsm_x4(smem_u32(qp + (r ^ 4) * QP_ROW + cof), qh[2 * kk][0], qh[2 * kk][1],
+                qh[2 * kk + 1][0], qh[2 * kk + 1][1]);
+    }
+  }
+  const float2 zz =
+      *reinterpret_cast<const float2*>(qp + 8 * QP_ROW + 8 * (CP == 2 ? (t4 & 1) : t4));
+  const float zs0 = zz.x * scale, zs1 = zz.y * scale;
+
+  // ---- S^T = codes_K . Q'^T over the chunk's 8*P tokens.  Tile pi goes
+  // to packed accumulator pi % NPK (columns 0..3 for pi < HALF, 4..7 for
+  // the partner pi >= HALF when CP = 2).  Independent HMMA chains: one per
+  // (accumulator, column half), and per channel-tile parity when few.
+  constexpr int HALF = NPAIR / 2;
+  constexpr bool KSPLIT = NPAIR <= 2;
+  constexpr int NCH = NPK * CP * (KSPLIT ? 2 : 1);
+  float chn[NCH][4];
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) chn[i][0] = chn[i][1] = chn[i][2] = chn[i][3] = 0.f;
+  if (!(dev_flags & 4)) {  // dev probe 4: skip the K side
+    const uint32_t kw = smem_u32(rec);
+    uint32_t kr[4][4];
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+      const int row = kc * 32 + lane;
+      ldsm_x4_t(kw + row * RB + ((j ^ swz(row, WN)) << 4), kr[kc][0], kr[kc][1], kr[kc][2],
+                kr[kc][3]);
+    }
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      const uint32_t rl = kr[kt / 2][2 * (kt % 2)], rh = kr[kt / 2][2 * (kt % 2) + 1];
+      const uint32_t rl8 = rl >> 8, rh8 = rh >> 8;
+#pragma unroll
+      for (int pi = 0; pi < NPAIR; ++pi) {
+        uint32_t af[4];
+#define BDK_KEXT(PI)                                 \
+  if (pi == PI) {                                    \
+    af[0] = ext_sub<BITS, (2 * PI) % P>(rl, rl8);     \
+    af[1] = ext_sub<BITS, (2 * PI + 1) % P>(rl, rl8); \
+    af[2] = ext_sub<BITS, (2 * PI) % P>(rh, rh8);     \
+    af[3] = ext_sub<BITS, (2 * PI + 1) % P>(rh, rh8); \
+  }
+        BDK_KEXT(0)
+        BDK_KEXT(1)
+        BDK_KEXT(2)
+        BDK_KEXT(3)
+#undef BDK_KEXT
+        const int f = (CP == 2 && pi >= HALF) ? 1 : 0;
+        const int ci = pi % NPK + NPK * (f + CP * (KSPLIT ? (kt & 1) : 0));
+        if (f)
+          mma16816(chn[ci], af, qh[CP == 2 ? kt : 0][0], qh[CP == 2 ? kt : 0][1]);
+        else
+          mma16816(chn[ci], af, qb[kt][0], qb[kt][1]);
+      }
+    }
+  }
+  float sacc[NPK][4];
+#pragma unroll
+  for (int i = 0; i < NPK; ++i)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      float x = chn[i][r];
+#pragma unroll
+      for (int k = 1; k < NCH / NPK; ++k) x += chn[i + k * NPK][r];
+      sacc[i][r] = x;
+    }
+  // ---- logits (log2 domain), online softmax
+  // S = S' 2^(24 - sh) + Z (rows gid / gid+8 hold fields 2i / 2i+1; the
+  // partner tile i + HALF has the same field shifts), in the log2 domain
+#pragma unroll
+  for (int i = 0; i < NPK; ++i) {
+    const float al = scale * (float)(1 << (24 - ((2 * i) % P) * BITS % 8));
+    const float ah = scale * (float)(1 << (24 - ((2 * i + 1) % P) * BITS % 8));
+    sacc[i][0] = fmaf(sacc[i][0], al, zs0);
+    sacc[i][1] = fmaf(sacc[i][1], al, zs1);
+    sacc[i][2] = fmaf(sacc[i][2], ah, zs0);
+    sacc[i][3] = fmaf(sacc[i][3], ah, zs1);
+  }
+  softmax_update<NPK>(sacc, st, o);
+  // ---- P' = P * s_t (V token scale folded), zero term, P'^T fragments
+  uint32_t pb[NPK][2];
+#pragma unroll
+  for (int i = 0; i < NPK; ++i) {
+    // V (scale, zero) of the tokens of rows gid / gid+8 (fields 2i / 2i+1
+    // of this lane's tile); the scale carries 2^(SH_REF - sh) of the
+    // field's subnormal shift
+    const int g0 = (8 * j + gid) * P;
+    const float2 pa = __half22float2(u2h(vpr[g0 + vtok[i][0]]));
+    const float2 pz = __half22float2(u2h(vpr[g0 + vtok[i][1]]));
+    const float2 sz0 = make_float2(
+        pa.x * (float)(1 << (SH_REF + 8)) / (float)(1 << (8 + ((2 * i) % P) * BITS % 8)), pa.y);
+    const float2 sz1 = make_float2(
+        pz.x * (float)(1 << (SH_REF + 8)) / (float)(1 << (8 + ((2 * i + 1) % P) * BITS % 8)),
+        pz.y);
+    st.z0 = fmaf(sacc[i][0], sz0.y, fmaf(sacc[i][2], sz1.y, st.z0));
+    st.z1 = fmaf(sacc[i][1], sz0.y, fmaf(sacc[i][3], sz1.y, st.z1));
+    pb[i][0] = movmatrix_t(pack_h2(sacc[i][0] * sz0.x, sacc[i][1] * sz0.x));
+    pb[i][1] = movmatrix_t(pack_h2(sacc[i][2] * sz1.x, sacc[i][3] * sz1.x));
+  }
+  // CP = 2: P'^T of tile i keeps only its column half (head columns n =
+  // gid after the transpose)
+  uint32_t pbh[CP == 2 ? NPK : 1][2];
+  if constexpr (CP == 2) {
+#pragma unroll
+    for (int i = 0; i < NPK; ++i) {
+      pbh[i][0] = gid >= 4 ? pb[i][0] : 0u;
+      pbh[i][1] = gid >= 4 ? pb[i][1] : 0u;
+      pb[i][0] = gid < 4 ? pb[i][0] : 0u;
+      pb[i][1] = gid < 4 ? pb[i][1] : 0u;
+    }
+  }
+  // ---- O^T += codes_V^T . P'^T
+  {
+    const uint32_t vw = smem_u32(rec + G.wbytes);
+    uint32_t vr[4][4];
+#pragma unroll
+    for (int vc = 0; vc < 4; ++vc) {
+      const int row = vc * 32 + lane;
+      ldsm_x4(vw + row * RB + ((j ^ swz(row, WN)) << 4), vr[vc][0], vr[vc][1], vr[vc][2],
+              vr[vc][3]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_s);  // ring slot + prep slot are free
+#pragma unroll
+    for (int mt = 0; mt < KT; ++mt) {
+      if (dev_flags & 8) break;  // dev probe 8: skip the V side
+      const uint32_t ra = vr[mt / 2][2 * (mt % 2)], rb = vr[mt / 2][2 * (mt % 2) + 1];
+      const uint32_t ra8 = ra >> 8, rb8 = rb >> 8;
+#pragma unroll
+      for (int pi = 0; pi < NPAIR; ++pi) {
+        uint32_t af[4];
+#define BDK_VEXT(PI)                                 \
+  if (pi == PI) {                                    \
+    af[0] = ext_sub<BITS, (2 * PI) % P>(ra, ra8);     \
+    af[1] = ext_sub<BITS, (2 * PI) % P>(rb, rb8);     \
+    af[2] = ext_sub<BITS, (2 * PI + 1) % P>(ra, ra8); \
+    af[3] = ext_sub<BITS, (2 * PI + 1) % P>(rb, rb8); \
+  }
+        BDK_VEXT(0)
+        BDK_VEXT(1)
+        BDK_VEXT(2)
+        BDK_VEXT(3)
+#undef BDK_VEXT
+        if (CP == 2 && pi >= HALF)
+          mma16816(o[mt], af, pbh[CP == 2 ? pi - HALF : 0][0], pbh[CP == 2 ? pi - HALF : 0][1]);
+        else
+          mma16816(o[mt], af, pb[pi % NPK][0], pb[pi % NPK][1]);
+      }
+    }
+  }
+}
+
+// Residual tokens [t_lo, t_hi) of `cell` (fp16 window, residual_attend,
+// attention.cpp:92-105), split over the NC consumer warps in 16-token tiles;
+// writes the appended token first if row rl0 falls in the range.
+template <int NC, int CP>
+__device__ __forceinline__ void consume_residual(const DevCache& c, const FastArgs& a, int cell,
+                                                 int t_lo, int t_hi, int rl0, bool app,
+                                                 float scale, Soft& st, float (&o)[OT][4]) {
+  const Geom& G = c.G;
+  const int ng = a.n_group;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, t4 = lane & 3;
+  constexpr int RT = 16 * NC;
+  const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
+  __half* rk = c.res_k + (size_t)cell * G.n_r * D;
+  __half* rv = c.res_v + (size_t)cell * G.n_r * D;
+      if (app && rl0 >= t_lo && rl0 < t_hi) {  // append_token (kvcache.cpp:170-182)
+    const __half* kn = a.k_new + (size_t)cell * D;
+    const __half* vn = a.v_new + (size_t)cell * D;
+    for (int i = threadIdx.x; i < D; i += NC * 32) {
+      rk[(size_t)rl0 * D + i] = kn[i];
+      rv[(size_t)rl0 * D + i] = vn[i];
+    }
+    named_bar(1, NC * 32);
+  }
+  uint32_t qb[KT][2];
+  {
+    const __half* qh = a.q + ((size_t)bidx * a.heads_q + (size_t)hk * ng + gid) * D;
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      qb[kt][0] = gid < ng ? *reinterpret_cast<const uint32_t*>(qh + kt * 16 + 2 * t4) : 0u;
+      qb[kt][1] = gid < ng ? *reinterpret_cast<const uint32_t*>(qh + kt * 16 + 8 + 2 * t4) : 0u;
+    }
+  }
+  for (int t0 = t_lo + 16 * warp; t0 < t_hi; t0 += RT) {
+    const bool v0 = t0 + gid < t_hi, v1 = t0 + gid + 8 < t_hi;
+    const __half* k0 = rk + (size_t)(t0 + gid) * D + 2 * t4;
+    const __half* k1 = k0 + 8 * D;
+    float sacc[1][4] = {{0.f, 0.f, 0.f, 0.f}};
+    uint32_t ka[KT][4];
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      ka[kt][0] = v0 ? *reinterpret_cast<const uint32_t*>(k0 + kt * 16) : 0u;
+      ka[kt][1] = v1 ? *reinterpret_cast<const uint32_t*>(k1 + kt * 16) : 0u;
+      ka[kt][2] = v0 ? *reinterpret_cast<const uint32_t*>(k0 + kt * 16 + 8) : 0u;
+      ka[kt][3] = v1 ? *reinterpret_cast<const uint32_t*>(k1 + kt * 16 + 8) : 0u;
+    }
+    // V rows in the natural [token][channel] fragment; movmatrix.trans
+    // turns each 8x8 block into the V^T A-fragment (channel rows)
+    const __half* w0 = rv + (size_t)(t0 + gid) * D + 2 * t4;
+    const __half* w1 = w0 + 8 * D;
+    uint32_t va[KT][4];
+#pragma unroll
+    for (int mt = 0; mt < KT; ++mt) {
+      va[mt][0] = v0 ? *reinterpret_cast<const uint32_t*>(w0 + mt * 16) : 0u;
+      va[mt][1] = v0 ? *reinterpret_cast<const uint32_t*>(w0 + mt * 16 + 8) : 0u;
+      va[mt][2] = v1 ? *reinterpret_cast<const uint32_t*>(w1 + mt * 16) : 0u;
+      va[mt][3] = v1 ? *reinterpret_cast<const uint32_t*>(w1 + mt * 16 + 8) : 0u;
+    }
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) mma16816(sacc[0], ka[kt], qb[kt][0], qb[kt][1]);
+    // CP = 2: columns 4..7 are the partner stream, which the residual
+    // tokens do not feed
+    const bool live = CP == 1 || t4 < 2;
+    sacc[0][0] = v0 && live ? sacc[0][0] * scale : -INFINITY;
+    sacc[0][1] = v0 && live ? sacc[0][1] * scale : -INFINITY;
+    sacc[0][2] = v1 && live ? sacc[0][2] * scale : -INFINITY;
+    sacc[0][3] = v1 && live ? sacc[0][3] * scale : -INFINITY;
+    softmax_update<1>(sacc, st, o);
+    const uint32_t pb0 = movmatrix_t(pack_h2(sacc[0][0], sacc[0][1]));
+    const uint32_t pb1 = movmatrix_t(pack_h2(sacc[0][2], sacc[0][3]));
+#pragma unroll
+    for (int mt = 0; mt < KT; ++mt) {
+      uint32_t af[4];
+      af[0] = movmatrix_t(va[mt][0]);
+      af[1] = movmatrix_t(va[mt][1]);
+      af[2] = movmatrix_t(va[mt][2]);
+      af[3] = movmatrix_t(va[mt][3]);
+      mma16816(o[mt], af, pb0, pb1);
+    }
   }
 }
 
@@ -655,172 +929,9 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
         if (lane == 0) mbar_arrive(&empty[s]);
         continue;
       }
-      const uint8_t* rec = ring + (size_t)s * REC;
-      const uint8_t* pp = prep + (size_t)s * L.prep_stride;
-      const uint8_t* qp = pp + kgr * QP_BYTES;
-      const uint32_t* vpr = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes + G.kp_bytes);
-      // Q'^T B fragments (ldmatrix of the [head][channel] rows; rows >= n_group
-      // are zero).  CP = 2: qh = the same heads in columns 4..7 (each lane's
-      // row address is r ^ 4, so columns 0..3 read the zero rows 4..7)
-      uint32_t qb[KT][2], qh[CP == 2 ? KT : 1][2];
-      {
-        const int mi = lane >> 3, r = lane & 7;
-#pragma unroll
-        for (int kk = 0; kk < KT / 2; ++kk) {
-          const int kt = 2 * kk + (mi >> 1);
-          const int cof = (kt * 16 + (mi & 1) * 8) * 2;
-          ldsm_x4(smem_u32(qp + r * QP_ROW + cof), qb[2 * kk][0], qb[2 * kk][1], qb[2 * kk + 1][0],
-                  qb[2 * kk + 1][1]);
-          if constexpr (CP == 2)
-            ldsm_x4(smem_u32(qp + (r ^ 4) * QP_ROW + cof), qh[2 * kk][0], qh[2 * kk][1],
-                    qh[2 * kk + 1][0], qh[2 * kk + 1][1]);
-        }
-      }
-      const float2 zz =
-          *reinterpret_cast<const float2*>(qp + 8 * QP_ROW + 8 * (CP == 2 ? (t4 & 1) : t4));
-      const float zs0 = zz.x * scale, zs1 = zz.y * scale;
-
-      // ---- S^T = codes_K . Q'^T over the chunk's 8*P tokens.  Tile pi goes
-      // to packed accumulator pi % NPK (columns 0..3 for pi < HALF, 4..7 for
-      // the partner pi >= HALF when CP = 2).  Independent HMMA chains: one per
-      // (accumulator, column half), and per channel-tile parity when few.
-      constexpr int HALF = NPAIR / 2;
-      constexpr bool KSPLIT = NPAIR <= 2;
-      constexpr int NCH = NPK * CP * (KSPLIT ? 2 : 1);
-      float chn[NCH][4];
-#pragma unroll
-      for (int i = 0; i < NCH; ++i) chn[i][0] = chn[i][1] = chn[i][2] = chn[i][3] = 0.f;
-      if (!(a.dev_flags & 4)) {  // dev probe 4: skip the K side
-        const uint32_t kw = smem_u32(rec);
-        uint32_t kr[4][4];
-#pragma unroll
-        for (int kc = 0; kc < 4; ++kc) {
-          const int row = kc * 32 + lane;
-          ldsm_x4_t(kw + row * RB + ((j ^ swz(row, WN)) << 4), kr[kc][0], kr[kc][1], kr[kc][2],
-                    kr[kc][3]);
-        }
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-          const uint32_t rl = kr[kt / 2][2 * (kt % 2)], rh = kr[kt / 2][2 * (kt % 2) + 1];
-          const uint32_t rl8 = rl >> 8, rh8 = rh >> 8;
-#pragma unroll
-          for (int pi = 0; pi < NPAIR; ++pi) {
-            uint32_t af[4];
-#define BDK_KEXT(PI)                                 \
-  if (pi == PI) {                                    \
-    af[0] = ext_sub<BITS, (2 * PI) % P>(rl, rl8);     \
-    af[1] = ext_sub<BITS, (2 * PI + 1) % P>(rl, rl8); \
-    af[2] = ext_sub<BITS, (2 * PI) % P>(rh, rh8);     \
-    af[3] = ext_sub<BITS, (2 * PI + 1) % P>(rh, rh8); \
-  }
-            BDK_KEXT(0)
-            BDK_KEXT(1)
-            BDK_KEXT(2)
-            BDK_KEXT(3)
-#undef BDK_KEXT
-            const int f = (CP == 2 && pi >= HALF) ? 1 : 0;
-            const int ci = pi % NPK + NPK * (f + CP * (KSPLIT ? (kt & 1) : 0));
-            if (f)
-              mma16816(chn[ci], af, qh[CP == 2 ? kt : 0][0], qh[CP == 2 ? kt : 0][1]);
-            else
-              mma16816(chn[ci], af, qb[kt][0], qb[kt][1]);
-          }
-        }
-      }
-      float sacc[NPK][4];
-#pragma unroll
-      for (int i = 0; i < NPK; ++i)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          float x = chn[i][r];
-#pragma unroll
-          for (int k = 1; k < NCH / NPK; ++k) x += chn[i + k * NPK][r];
-          sacc[i][r] = x;
-        }
-      // ---- logits (log2 domain), online softmax
-      // S = S' 2^(24 - sh) + Z (rows gid / gid+8 hold fields 2i / 2i+1; the
-      // partner tile i + HALF has the same field shifts), in the log2 domain
-#pragma unroll
-      for (int i = 0; i < NPK; ++i) {
-        const float al = scale * (float)(1 << (24 - ((2 * i) % P) * BITS % 8));
-        const float ah = scale * (float)(1 << (24 - ((2 * i + 1) % P) * BITS % 8));
-        sacc[i][0] = fmaf(sacc[i][0], al, zs0);
-        sacc[i][1] = fmaf(sacc[i][1], al, zs1);
-        sacc[i][2] = fmaf(sacc[i][2], ah, zs0);
-        sacc[i][3] = fmaf(sacc[i][3], ah, zs1);
-      }
-      softmax_update<NPK>(sacc, st, o);
-      // ---- P' = P * s_t (V token scale folded), zero term, P'^T fragments
-      uint32_t pb[NPK][2];
-#pragma unroll
-      for (int i = 0; i < NPK; ++i) {
-        // V (scale, zero) of the tokens of rows gid / gid+8 (fields 2i / 2i+1
-        // of this lane's tile); the scale carries 2^(SH_REF - sh) of the
-        // field's subnormal shift
-        const int g0 = (8 * j + gid) * P;
-        const float2 pa = __half22float2(u2h(vpr[g0 + vtok[i][0]]));
-        const float2 pz = __half22float2(u2h(vpr[g0 + vtok[i][1]]));
-        const float2 sz0 = make_float2(
-            pa.x * (float)(1 << (SH_REF + 8)) / (float)(1 << (8 + ((2 * i) % P) * BITS % 8)), pa.y);
-        const float2 sz1 = make_float2(
-            pz.x * (float)(1 << (SH_REF + 8)) / (float)(1 << (8 + ((2 * i + 1) % P) * BITS % 8)),
-            pz.y);
-        st.z0 = fmaf(sacc[i][0], sz0.y, fmaf(sacc[i][2], sz1.y, st.z0));
-        st.z1 = fmaf(sacc[i][1], sz0.y, fmaf(sacc[i][3], sz1.y, st.z1));
-        pb[i][0] = movmatrix_t(pack_h2(sacc[i][0] * sz0.x, sacc[i][1] * sz0.x));
-        pb[i][1] = movmatrix_t(pack_h2(sacc[i][2] * sz1.x, sacc[i][3] * sz1.x));
-      }
-      // CP = 2: P'^T of tile i keeps only its column half (head columns n =
-      // gid after the transpose)
-      uint32_t pbh[CP == 2 ? NPK : 1][2];
-      if constexpr (CP == 2) {
-#pragma unroll
-        for (int i = 0; i < NPK; ++i) {
-          pbh[i][0] = gid >= 4 ? pb[i][0] : 0u;
-          pbh[i][1] = gid >= 4 ? pb[i][1] : 0u;
-          pb[i][0] = gid < 4 ? pb[i][0] : 0u;
-          pb[i][1] = gid < 4 ? pb[i][1] : 0u;
-        }
-      }
-      // ---- O^T += codes_V^T . P'^T
-      {
-        const uint32_t vw = smem_u32(rec + G.wbytes);
-        uint32_t vr[4][4];
-#pragma unroll
-        for (int vc = 0; vc < 4; ++vc) {
-          const int row = vc * 32 + lane;
-          ldsm_x4(vw + row * RB + ((j ^ swz(row, WN)) << 4), vr[vc][0], vr[vc][1], vr[vc][2],
-                  vr[vc][3]);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);  // ring slot + prep slot are free
-#pragma unroll
-        for (int mt = 0; mt < KT; ++mt) {
-          if (a.dev_flags & 8) break;  // dev probe 8: skip the V side
-          const uint32_t ra = vr[mt / 2][2 * (mt % 2)], rb = vr[mt / 2][2 * (mt % 2) + 1];
-          const uint32_t ra8 = ra >> 8, rb8 = rb >> 8;
-#pragma unroll
-          for (int pi = 0; pi < NPAIR; ++pi) {
-            uint32_t af[4];
-#define BDK_VEXT(PI)                                 \
-  if (pi == PI) {                                    \
-    af[0] = ext_sub<BITS, (2 * PI) % P>(ra, ra8);     \
-    af[1] = ext_sub<BITS, (2 * PI) % P>(rb, rb8);     \
-    af[2] = ext_sub<BITS, (2 * PI + 1) % P>(ra, ra8); \
-    af[3] = ext_sub<BITS, (2 * PI + 1) % P>(rb, rb8); \
-  }
-            BDK_VEXT(0)
-            BDK_VEXT(1)
-            BDK_VEXT(2)
-            BDK_VEXT(3)
-#undef BDK_VEXT
-            if (CP == 2 && pi >= HALF)
-              mma16816(o[mt], af, pbh[CP == 2 ? pi - HALF : 0][0], pbh[CP == 2 ? pi - HALF : 0][1]);
-            else
-              mma16816(o[mt], af, pb[pi % NPK][0], pb[pi % NPK][1]);
-          }
-        }
-      }
+      consume_block<BITS, WN, CP>(ring + (size_t)s * REC,
+                                  prep + (size_t)s * L.prep_stride + kgr * QP_BYTES, G, j, scale,
+                                  vtok, st, o, &empty[s], a.dev_flags);
     }
 
     it = it_end;
@@ -828,7 +939,6 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     // ---------------- residual window (fp16), append fused.  Residual unit r
     // of a cell covers tokens [r*RT, (r+1)*RT) (RT = 16 per consumer warp);
     // the CTA whose range holds row res_len writes the new token there.
-    int res_app = -1;  // res_len before the append, if this CTA appended
     float oscale_seg = oscale;
     if (seg_end > res_begin && !a.skip_residual) {
       // the packed-block O is held at scale 2^(SH_REF - 24) (subnormal-mode
@@ -842,80 +952,12 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       }
       oscale_seg = 1.f;
       constexpr int RT = 16 * NC;
-      const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
-      __half* rk = c.res_k + (size_t)cell * G.n_r * D;
-      __half* rv = c.res_v + (size_t)cell * G.n_r * D;
       const int rl0 = c.res_len[cell];
       const bool app = a.k_new != nullptr;
       const int rlen = rl0 + (app ? 1 : 0);
       const int t_lo = (int)(max(u, res_begin) - res_begin) * RT;
       const int t_hi = min(rlen, (int)(seg_end - res_begin) * RT);
-      if (app && rl0 >= t_lo && rl0 < t_hi) {  // append_token (kvcache.cpp:170-182)
-        const __half* kn = a.k_new + (size_t)cell * D;
-        const __half* vn = a.v_new + (size_t)cell * D;
-        for (int i = threadIdx.x; i < D; i += NC * 32) {
-          rk[(size_t)rl0 * D + i] = kn[i];
-          rv[(size_t)rl0 * D + i] = vn[i];
-        }
-        named_bar(1, NC * 32);
-        res_app = rl0;
-      }
-      uint32_t qb[KT][2];
-      {
-        const __half* qh = a.q + ((size_t)bidx * a.heads_q + (size_t)hk * ng + gid) * D;
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-          qb[kt][0] = gid < ng ? *reinterpret_cast<const uint32_t*>(qh + kt * 16 + 2 * t4) : 0u;
-          qb[kt][1] = gid < ng ? *reinterpret_cast<const uint32_t*>(qh + kt * 16 + 8 + 2 * t4) : 0u;
-        }
-      }
-      for (int t0 = t_lo + 16 * warp; t0 < t_hi; t0 += RT) {
-        const bool v0 = t0 + gid < t_hi, v1 = t0 + gid + 8 < t_hi;
-        const __half* k0 = rk + (size_t)(t0 + gid) * D + 2 * t4;
-        const __half* k1 = k0 + 8 * D;
-        float sacc[1][4] = {{0.f, 0.f, 0.f, 0.f}};
-        uint32_t ka[KT][4];
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-          ka[kt][0] = v0 ? *reinterpret_cast<const uint32_t*>(k0 + kt * 16) : 0u;
-          ka[kt][1] = v1 ? *reinterpret_cast<const uint32_t*>(k1 + kt * 16) : 0u;
-          ka[kt][2] = v0 ? *reinterpret_cast<const uint32_t*>(k0 + kt * 16 + 8) : 0u;
-          ka[kt][3] = v1 ? *reinterpret_cast<const uint32_t*>(k1 + kt * 16 + 8) : 0u;
-        }
-        // V rows in the natural [token][channel] fragment; movmatrix.trans
-        // turns each 8x8 block into the V^T A-fragment (channel rows)
-        const __half* w0 = rv + (size_t)(t0 + gid) * D + 2 * t4;
-        const __half* w1 = w0 + 8 * D;
-        uint32_t va[KT][4];
-#pragma unroll
-        for (int mt = 0; mt < KT; ++mt) {
-          va[mt][0] = v0 ? *reinterpret_cast<const uint32_t*>(w0 + mt * 16) : 0u;
-          va[mt][1] = v0 ? *reinterpret_cast<const uint32_t*>(w0 + mt * 16 + 8) : 0u;
-          va[mt][2] = v1 ? *reinterpret_cast<const uint32_t*>(w1 + mt * 16) : 0u;
-          va[mt][3] = v1 ? *reinterpret_cast<const uint32_t*>(w1 + mt * 16 + 8) : 0u;
-        }
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) mma16816(sacc[0], ka[kt], qb[kt][0], qb[kt][1]);
-        // CP = 2: columns 4..7 are the partner stream, which the residual
-        // tokens do not feed
-        const bool live = CP == 1 || t4 < 2;
-        sacc[0][0] = v0 && live ? sacc[0][0] * scale : -INFINITY;
-        sacc[0][1] = v0 && live ? sacc[0][1] * scale : -INFINITY;
-        sacc[0][2] = v1 && live ? sacc[0][2] * scale : -INFINITY;
-        sacc[0][3] = v1 && live ? sacc[0][3] * scale : -INFINITY;
-        softmax_update<1>(sacc, st, o);
-        const uint32_t pb0 = movmatrix_t(pack_h2(sacc[0][0], sacc[0][1]));
-        const uint32_t pb1 = movmatrix_t(pack_h2(sacc[0][2], sacc[0][3]));
-#pragma unroll
-        for (int mt = 0; mt < KT; ++mt) {
-          uint32_t af[4];
-          af[0] = movmatrix_t(va[mt][0]);
-          af[1] = movmatrix_t(va[mt][1]);
-          af[2] = movmatrix_t(va[mt][2]);
-          af[3] = movmatrix_t(va[mt][3]);
-          mma16816(o[mt], af, pb0, pb1);
-        }
-      }
+      consume_residual<NC, CP>(c, a, cell, t_lo, t_hi, rl0, app, scale, st, o);
     }
 
     // ---------------- segment partial -> slot (CTA + cell), completion count
@@ -938,7 +980,9 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     }
     named_bar(1, NC * 32);
     if (tr && threadIdx.x == 0) tr[10] = globaltimer();
-    if (*flag) merge_cell<NC>(a, G, cell, lo, hi, merge_sm, tr);
+    if (*flag)
+      merge_cell<NC>(a, G, cell, a.slots + (size_t)(lo + cell) * stride_slot, hi - lo + 1, merge_sm,
+                     tr);
     if (tr && threadIdx.x == 0) {
       tr[5] = globaltimer();
       tr[6] = (unsigned long long)(*flag);
@@ -954,6 +998,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     u = seg_end;
   }
 }
+
 
 }  // namespace
 
@@ -1008,6 +1053,12 @@ static Variant fast_kernel(const Geom& G, int ng) {
     BDK_SEL(2, 4, 8, 1, 2) BDK_SEL(4, 4, 8, 1, 2)
   } else if (v == 3) {
     BDK_SEL(2, 4, 6, 1, 3) BDK_SEL(4, 4, 9, 1, 3)
+  } else if (v == 4) {  // ring depth probes (2 CTAs per SM)
+    BDK_SEL(2, 4, 3, 2, 1) BDK_SEL(4, 4, 3, 2, 1)
+  } else if (v == 5) {
+    BDK_SEL(2, 4, 5, 2, 1) BDK_SEL(4, 4, 5, 2, 1)
+  } else if (v == 6) {
+    BDK_SEL(2, 4, 2, 2, 1) BDK_SEL(4, 4, 2, 2, 1)
   }
   BDK_SEL(2, 1, 4, 2, 1) BDK_SEL(2, 2, 4, 2, 1) BDK_SEL(2, 4, 4, 2, 1) BDK_SEL(2, 8, 4, 1, 1)
   BDK_SEL(4, 1, 4, 2, 1) BDK_SEL(4, 2, 4, 2, 1) BDK_SEL(4, 4, 4, 2, 1) BDK_SEL(4, 8, 4, 1, 1)
