@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libbitdecode_b200.so")
 SOURCES = ["bdk_kernels.cu", "bdk_decode_fast.cu", "bdk_api.cu"]
-HEADERS = ["bdk_common.cuh", "bdk_frag.cuh", "bdk_qpack.cuh", "bdk_launch.h"]
+HEADERS = ["bdk_common.cuh", "bdk_frag.cuh", "bdk_qpack.cuh", "bdk_qpack_fast.cuh", "bdk_launch.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",

@@ -34,7 +34,10 @@
 
 #include "bdk_launch.h"
 #include "bdk_frag.cuh"
+#include <cstdlib>
+
 #include "bdk_qpack.cuh"
+#include "bdk_qpack_fast.cuh"
 
 namespace bdk {
 
@@ -729,6 +732,19 @@ int max_ctas_per_sm(const Geom&) { return 3; }
 template <int BITS>
 static cudaError_t prefill_bits(const DevCache& c, const __half* k, const __half* v, int len,
                                 int cell_begin, int n_cells, cudaStream_t s) {
+  if constexpr (BITS != 16) {
+    static const bool fast_off = getenv("BDK_QPACK_FAST") && atoi(getenv("BDK_QPACK_FAST")) == 0;
+    if (qpack_fast_ok(c.G) && !fast_off) {
+      const QfSmem L = qf_layout(c.G);
+      auto kern = qpack_fast_kernel<BITS>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(L.total));
+      if (e != cudaSuccess) return e;
+      dim3 grid((len / c.G.n_r) * (c.G.n_r / QF_D) + 1, n_cells, 2);
+      kern<<<grid, QF_THREADS, L.total, s>>>(c, k, v, len, cell_begin);
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = (size_t)c.G.n_r * c.G.d;
   auto kern = prefill_kernel<BITS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

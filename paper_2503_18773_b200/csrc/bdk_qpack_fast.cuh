@@ -1,0 +1,298 @@
+// bdk_qpack_fast.cuh -- tile-staged fused quantize-and-pack (sm_100a).
+//
+// Same bit-exact result as qpack_block (bdk_qpack.cuh; kvcache.cpp:184-206,
+// quant.cpp:18-93, layout.cpp:45-61) for the BASELINE geometry (d = 128,
+// group 128, KChannel K, token-wise V), restructured for HBM throughput:
+//
+//   * one CTA per (block, 128-token group, cell, tensor): K and V of a block
+//     are independent, and with group 128 so are the 128-token halves of an
+//     N_r = 256 block, so a CTA stages ONE [128][128] fp16 tile (32 KB) with
+//     a single TMA bulk copy and four CTAs per SM overlap their loads with
+//     each other's arithmetic;
+//   * group (min, max) over the staged tile with half2 min/max (exact on
+//     binary16 values; the sign of a zero extremum is taken from the first
+//     zero in scan order, the reference's strict-compare tie rule);
+//   * code = rint((x - z) / s) via x * rcp(s): the product is within 2^-22
+//     relative of the quotient, so it rounds to the same integer unless it
+//     lies within 1e-4 of a half-integer -- those (rare) elements take the
+//     exact IEEE division (__fdiv_rn), so every code equals the reference's;
+//   * the params are assembled in shared memory and written with one TMA
+//     bulk store; the words go out as 16-byte stores in the record's
+//     (swizzled) row layout.
+#pragma once
+#include "bdk_common.cuh"
+#include "bdk_qpack.cuh"
+
+namespace bdk {
+
+constexpr int QF_D = 128;        // head_dim served
+constexpr int QF_THREADS = 256;  // threads per CTA
+
+__host__ __device__ inline bool qpack_fast_ok(const Geom& G) {
+  return G.d == QF_D && G.g == QF_D && G.k_axis == 0 &&
+         (G.bits == 2 || G.bits == 4 || G.bits == 8) && G.n_r % QF_D == 0 && G.warp_n <= 8;
+}
+
+struct QfSmem {
+  uint32_t tile, out, pout, fs, part, bar, total;
+};
+
+__host__ __device__ inline QfSmem qf_layout(const Geom& G) {
+  (void)G;
+  QfSmem L;
+  L.tile = 0;
+  L.out = (uint32_t)(QF_D * QF_D * 2);  // staged fp16 tile [128 tokens][128]
+  L.pout = L.out;                        // (words go straight to global)
+  L.fs = L.pout + QF_D * 4;              // u32 params of the tile (record layout)
+  L.part = L.fs + QF_D * 16;             // float4 (s, z, 1/s, -) per group
+  L.bar = L.part + 2u * 4u * 64u * 4u;   // K partial half2 (lo, hi) per part
+  L.total = L.bar + 16u;
+  return L;
+}
+
+__device__ __forceinline__ void tma_bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+
+// One word with the exact IEEE quotient (quant.cpp:30-38): the rare case of a
+// product within 1e-4 of a half-integer.  Out of line to keep the fast path
+// small.
+template <int BITS>
+__device__ __noinline__ uint32_t exact_word(const __half* tile, const float4* fs, int tsr, int tw,
+                                            int ch, float4 pk, int interleave) {
+  constexpr int P = 16 / BITS;
+  const float qmax = static_cast<float>((1u << BITS) - 1u);
+  uint32_t word = 0;
+  for (int p = 0; p < P; ++p) {
+    const int t = tw + pos_token(p, P, interleave);
+    if (tsr != 0) pk = fs[t];
+    word |= quant_code(__half2float(tile[(size_t)t * QF_D + ch]), pk.x, pk.y, qmax) << (p * BITS);
+  }
+  return word;
+}
+
+// codes + pack of one 128-token tile (tokens [hf*128, hf*128+128) of the
+// block): item (chunk j of the tile, channel pair cp) -> the 8 words (8*P
+// tokens) of channels 2cp and 2cp+1, stored as 16 bytes each at their
+// swizzled row position in the record; one half2 load feeds both channels.
+// TOKEN_PARAMS: V (a (scale, zero) per token) else K (per channel; the tile
+// is one 128-token group).  Codes need no clamp here: z = lo exactly and
+// s >= (hi - lo) / qmax * (1 - 2^-11), so every in-group quotient lies in
+// [0, qmax + 0.5).
+template <int BITS, bool TOKEN_PARAMS>
+__device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, uint8_t* words,
+                                        const Geom& G, int hf) {
+  constexpr int P = 16 / BITS;
+  constexpr int CPT = QF_D / (8 * P);  // 16-byte chunks per row in one tile
+  // SPLIT threads share a chunk (4 / SPLIT word pairs each) so that all
+  // QF_THREADS threads have an item at 2-bit too
+  constexpr int SPLIT = QF_THREADS / (CPT * (QF_D / 2)) < 1 ? 1 : QF_THREADS / (CPT * (QF_D / 2));
+  constexpr int NP = 4 / SPLIT;  // u32 word pairs per item
+  const __half2* tile2 = reinterpret_cast<const __half2*>(tile);
+  const int wn = G.warp_n, rb = 16 * wn;
+  int tok[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) tok[p] = pos_token(p, P, G.interleave);
+  for (int item = threadIdx.x; item < SPLIT * CPT * (QF_D / 2); item += QF_THREADS) {
+    const int sp = item / (CPT * (QF_D / 2));
+    const int jl = (item / (QF_D / 2)) % CPT, cp = item % (QF_D / 2);
+    const int t0 = jl * 8 * P + sp * NP * 2 * P;  // first token (tile-relative)
+    const int j = hf * CPT + jl;                   // chunk index in the row
+    float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa;
+    if (!TOKEN_PARAMS) {
+      pa = fs[2 * cp];
+      pb = fs[2 * cp + 1];
+    }
+    uint32_t w0[NP], w1[NP];
+#pragma unroll
+    for (int i2 = 0; i2 < NP; ++i2) {
+      uint32_t p0 = 0, p1 = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int tw = t0 + (i2 * 2 + h) * P;  // first token of the word
+        uint32_t a0 = 0, a1 = 0;
+        bool tie = false;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const int t = tw + tok[p];
+          if (TOKEN_PARAMS) pa = pb = fs[t];
+          const float2 x = __half22float2(tile2[(size_t)t * 64 + cp]);
+          const float q0 = __fmul_rn(__fsub_rn(x.x, pa.y), pa.z);
+          const float q1 = __fmul_rn(__fsub_rn(x.y, pb.y), pb.z);
+          const float r0 = rintf(q0), r1 = rintf(q1);
+          tie |= (fabsf(q0 - r0) > 0.4999f) | (fabsf(q1 - r1) > 0.4999f);
+          a0 += __float2uint_rn(r0) << (p * BITS);
+          a1 += __float2uint_rn(r1) << (p * BITS);
+        }
+        if (__any_sync(0xffffffffu, tie) && tie) {
+          a0 = exact_word<BITS>(tile, fs, TOKEN_PARAMS, tw, 2 * cp, pa, G.interleave);
+          a1 = exact_word<BITS>(tile, fs, TOKEN_PARAMS, tw, 2 * cp + 1, pb, G.interleave);
+        }
+        p0 |= a0 << (16 * h);
+        p1 |= a1 << (16 * h);
+      }
+      w0[i2] = p0;
+      w1[i2] = p1;
+    }
+    const int ca = 2 * cp, cb = 2 * cp + 1;
+    uint8_t* da = words + (size_t)ca * rb + ((j ^ swz(ca, wn)) << 4) + sp * NP * 4;
+    uint8_t* db = words + (size_t)cb * rb + ((j ^ swz(cb, wn)) << 4) + sp * NP * 4;
+    if constexpr (NP == 4) {
+      *reinterpret_cast<uint4*>(da) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+      *reinterpret_cast<uint4*>(db) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+    } else if constexpr (NP == 2) {
+      *reinterpret_cast<uint2*>(da) = make_uint2(w0[0], w0[1]);
+      *reinterpret_cast<uint2*>(db) = make_uint2(w1[0], w1[1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NP; ++i) {
+        reinterpret_cast<uint32_t*>(da)[i] = w0[i];
+        reinterpret_cast<uint32_t*>(db)[i] = w1[i];
+      }
+    }
+  }
+}
+
+// grid (nb * H + 1, cells, 2) with H = N_r / 128 tiles per block: x < nb*H
+// packs tile x % H of block x / H of cell (cell_begin + y), tensor z (0 = K,
+// 1 = V); x == nb*H, z == 0 copies the residual tail and sets the cell's
+// lengths (prefill_kernel's tail branch).
+template <int BITS>
+__global__ void __launch_bounds__(QF_THREADS) qpack_fast_kernel(DevCache c, const __half* k,
+                                                                const __half* v, int len,
+                                                                int cell_begin) {
+  const float qmax = static_cast<float>((1u << BITS) - 1u);
+  extern __shared__ __align__(128) uint8_t smem[];
+  const Geom& G = c.G;
+  const int cell = cell_begin + blockIdx.y;
+  const int nb = len / G.n_r;
+  const int H = G.n_r / QF_D;
+  const int tsr = blockIdx.z;
+  if ((int)blockIdx.x >= nb * H) {  // residual tail + lengths
+    if (tsr != 0) return;
+    const int tail = len - nb * G.n_r;
+    const size_t src = (size_t)blockIdx.y * len * QF_D + (size_t)nb * G.n_r * QF_D;
+    const size_t dst = (size_t)cell * G.n_r * QF_D;
+    for (int i = threadIdx.x; i < tail * QF_D; i += blockDim.x) {
+      c.res_k[dst + i] = k[src + i];
+      c.res_v[dst + i] = v[src + i];
+    }
+    if (threadIdx.x == 0) {
+      c.packed_blocks[cell] = nb;
+      c.res_len[cell] = tail;
+    }
+    return;
+  }
+  const int blk = blockIdx.x / H, hf = blockIdx.x % H;
+  const QfSmem L = qf_layout(G);
+  const __half* tile = reinterpret_cast<const __half*>(smem + L.tile);
+  const __half2* tile2 = reinterpret_cast<const __half2*>(tile);
+  uint32_t* pout = reinterpret_cast<uint32_t*>(smem + L.pout);
+  float4* fs = reinterpret_cast<float4*>(smem + L.fs);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  constexpr uint32_t TILE_BYTES = QF_D * QF_D * 2;
+  const __half* src = (tsr ? v : k) + (size_t)blockIdx.y * len * QF_D +
+                      ((size_t)blk * G.n_r + (size_t)hf * QF_D) * QF_D;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(bar, TILE_BYTES);
+    tma_bulk_g2s(smem + L.tile, src, TILE_BYTES, bar, policy_evict_first());
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+
+  const int tid = threadIdx.x;
+  if (tsr == 0) {
+    // ---- K: KChannel group = this tile's 128 tokens of one channel, param
+    // [gr = hf][c].  Thread (channel pair, quarter) scans 32 tokens with half2
+    // min/max; the first-zero lookup (tie rule) runs only for a zero extremum.
+    __half2* plo = reinterpret_cast<__half2*>(smem + L.part);  // [part][cp]
+    __half2* phi = plo + 4 * 64;
+    {
+      const int cp = tid % 64, part = tid / 64;
+      const int t0 = part * 32;
+      __half2 lo = tile2[(size_t)t0 * 64 + cp], hi = lo;
+#pragma unroll 8
+      for (int t = t0 + 1; t < t0 + 32; ++t) {
+        const __half2 x = tile2[(size_t)t * 64 + cp];
+        lo = __hmin2(lo, x);
+        hi = __hmax2(hi, x);
+      }
+      plo[part * 64 + cp] = lo;
+      phi[part * 64 + cp] = hi;
+    }
+    __syncthreads();
+    if (tid < QF_D) {
+      const int ch = tid;
+      float lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const __half2 l2 = plo[p * 64 + ch / 2], h2 = phi[p * 64 + ch / 2];
+        lo = fminf(lo, __half2float((ch & 1) ? __high2half(l2) : __low2half(l2)));
+        hi = fmaxf(hi, __half2float((ch & 1) ? __high2half(h2) : __low2half(h2)));
+      }
+      if (lo == 0.f || hi == 0.f) {  // sign of the first zero in token order
+        for (int t = 0; t < QF_D; ++t) {
+          const float x = __half2float(tile[(size_t)t * QF_D + ch]);
+          if (x == 0.f) {
+            if (lo == 0.f) lo = x;
+            if (hi == 0.f) hi = x;
+            break;
+          }
+        }
+      }
+      float s, z;
+      group_params(lo, hi, qmax, s, z);
+      fs[ch] = make_float4(s, z, __frcp_rn(s), 0.f);
+      pout[ch] = param_u32(s, z);
+    }
+  } else {
+    // ---- V: token groups (the 128 channels of one token), param [t].
+    // Thread per token; the scan is staggered by token so the 32 rows of a
+    // warp hit 32 distinct banks.
+    if (tid < QF_D) {
+      const int t = tid;
+      const __half2* row = tile2 + (size_t)t * 64;
+      __half2 lo = row[t & 63], hi = lo;
+#pragma unroll 8
+      for (int i = 1; i < 64; ++i) {
+        const __half2 x = row[(i + t) & 63];
+        lo = __hmin2(lo, x);
+        hi = __hmax2(hi, x);
+      }
+      float flo = fminf(__low2float(lo), __high2float(lo));
+      float fhi = fmaxf(__low2float(hi), __high2float(hi));
+      if (flo == 0.f || fhi == 0.f) {  // sign of the first zero in channel order
+        for (int ch = 0; ch < QF_D; ++ch) {
+          const float x = __half2float(tile[(size_t)t * QF_D + ch]);
+          if (x == 0.f) {
+            if (flo == 0.f) flo = x;
+            if (fhi == 0.f) fhi = x;
+            break;
+          }
+        }
+      }
+      float s, z;
+      group_params(flo, fhi, qmax, s, z);
+      fs[t] = make_float4(s, z, __frcp_rn(s), 0.f);
+      pout[t] = param_u32(s, z);
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
+  uint8_t* rec = c.records + ((size_t)cell * G.max_blocks + blk) * G.rec_bytes;
+  if (threadIdx.x == 0) {  // this tile's params: 128 u32, contiguous in the record
+    tma_bulk_s2g(rec + 2 * G.wbytes + (tsr ? G.kp_bytes : 0) + hf * QF_D * 4, pout, QF_D * 4);
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+  }
+  if (tsr == 0)
+    qf_pack<BITS, false>(tile, fs, rec, G, hf);
+  else
+    qf_pack<BITS, true>(tile, fs, rec + G.wbytes, G, hf);
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
+}  // namespace bdk

@@ -42,6 +42,26 @@ def prefill_data(c: Case, gauss: O.Gauss):
     return k, v
 
 
+def adversarial_data(c: Case, seed: int):
+    """binary16 data that stresses the exactness rules of quantize_tile
+    (quant.cpp:18-93): a coarse grid (exact .5 quotients -> the ties-to-even
+    path), zeros of both signs as group extrema (the first-zero sign rule),
+    constant groups (scale clamped to kMinScale), and a large-magnitude
+    channel."""
+    rng = np.random.default_rng(seed)
+    shape = (c.batch, c.heads_kv, c.prefill, D)
+    grid = np.array([-2.0, -1.5, -1.0, -0.5, -0.0, 0.0, 0.5, 1.0, 1.5, 2.0], np.float32)
+    k = grid[rng.integers(0, grid.size, shape)]
+    v = grid[rng.integers(0, grid.size, shape)]
+    k[..., 3] = 0.0                       # a channel of +0
+    k[..., 5] = -0.0                      # a channel of -0
+    k[..., 7] = 7.25                      # a constant channel
+    k[..., 9] = rng.normal(0, 300, shape[:-1]).astype(np.float16).astype(np.float32)
+    v[:, :, ::17, :] = -0.0               # all-zero tokens
+    v[:, :, 1::19, :] = 3.0               # constant tokens
+    return k.astype(np.float16).astype(np.float32), v.astype(np.float16).astype(np.float32)
+
+
 def step_data(c: Case, gauss: O.Gauss):
     q = gauss.rounded(c.batch * c.heads_q * D).reshape(c.batch, c.heads_q, D)
     kn = gauss.rounded(c.batch * c.heads_kv * D).reshape(c.batch, c.heads_kv, D)

@@ -10,7 +10,7 @@ include/bitdecode_b200.h).  Tolerances (stated per DESIGN.md "Numerics"):
 import numpy as np
 import pytest
 
-from tests._cases import D, Case, errors, oracle_cache, prefill_data, step_data
+from tests._cases import D, Case, adversarial_data, errors, oracle_cache, prefill_data, step_data
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -95,6 +95,28 @@ def test_prefill_packs_bit_exact(bits, warp_n, g, axis):
     gauss = O.Gauss(c.seed)
     k, v = prefill_data(c, gauss)
     assert_same_cache(c, gpu_cache(c, k, v), oracle_cache(c, k, v))
+
+
+@pytest.mark.parametrize("bits,warp_n", [(4, 4), (2, 4), (2, 2), (4, 8), (8, 8)])
+def test_prefill_adversarial_bit_exact(bits, warp_n):
+    c = Case(bits=bits, warp_n=warp_n, heads_kv=2, batch=1,
+             prefill=4 * (8 * warp_n * (16 // bits)) + 5, seed=bits + warp_n)
+    k, v = adversarial_data(c, c.seed)
+    assert_same_cache(c, gpu_cache(c, k, v), oracle_cache(c, k, v))
+
+
+def test_reset_then_prefill_again():
+    from oracle import oracle as O
+    c = Case(bits=2, warp_n=4, heads_kv=2, batch=2, prefill=3 * 256 + 11, seed=21)
+    k, v = prefill_data(c, O.Gauss(c.seed))
+    gc = gpu_cache(c, k, v)
+    k2, v2 = prefill_data(c, O.Gauss(c.seed + 1))
+    gc.reset()
+    for b in range(c.batch):
+        for h in range(c.heads_kv):
+            assert gc.packed_len(b, h) == 0 and gc.res_len(b, h) == 0
+    gc.prefill_all(torch.from_numpy(k2).cuda().half(), torch.from_numpy(v2).cuda().half())
+    assert_same_cache(c, gc, oracle_cache(c, k2, v2))
 
 
 def test_identity_permutation_packs_bit_exact():

@@ -221,3 +221,23 @@ def test_oracle_naive_attention_equals_reference():  # oracle.cpp:12-37
     k = g.rounded(300 * 64).reshape(300, 64)
     v = g.rounded(300 * 64).reshape(300, 64)
     assert np.array_equal(O.naive_attention(q, k, v), O.ref_naive_attention(q, k, v))
+
+
+@needs_ref
+@pytest.mark.parametrize("bits,wn", [(4, 4), (2, 4), (2, 2), (4, 8), (8, 8)])
+def test_oracle_blocks_equal_live_reference_on_adversarial_data(bits, wn):
+    """The oracle's quantize+pack equals the reference's on data built to hit
+    exact .5 quotients, signed-zero extrema and constant groups (the inputs
+    of test_gpu_parity.test_prefill_adversarial_bit_exact)."""
+    from tests._cases import Case, adversarial_data
+    c = Case(bits=bits, warp_n=wn, heads_kv=2, batch=1, prefill=4 * (8 * wn * (16 // bits)) + 5,
+             seed=bits + wn)
+    k, v = adversarial_data(c, c.seed)
+    rc = O.RefCache(1, 2, 128, wn, bits, 0, 128, True)
+    oc = O.OracleCache(1, 2, 128, wn, bits, 0, 128, True, max_tokens=c.prefill + 8)
+    for h in range(2):
+        rc.prefill(0, h, k[0, h], v[0, h])
+        oc.prefill(0, h, k[0, h], v[0, h])
+        for i in range(rc.packed_len(0, h) // rc.n_r):
+            for x, y in zip(rc.block(0, h, i), oc.block(0, h, i)):
+                assert np.array_equal(x, y)
