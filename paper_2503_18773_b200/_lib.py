@@ -84,12 +84,16 @@ def load() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    # BDK_LIB (dev A/B runs): another build of the same C-ABI
+    path = os.environ.get("BDK_LIB") or LIB_PATH
+    if not os.path.exists(path):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2503_18773_b200.build` "
+            f"{path} is missing: build it with `python -m paper_2503_18773_b200.build` "
             "(nvcc, sm_100a).  There is no CPU fallback.")
-    L = C.CDLL(LIB_PATH)
+    L = C.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
+        if path != LIB_PATH and not hasattr(L, name):
+            continue
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args

@@ -247,6 +247,13 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
   a.unit_off = c->unit_off;
   a.unit_nb = c->unit_off + cells + 1;
   a.total_units = T;
+  {
+    bool uni = true;
+    for (int i = 1; i < cells && uni; ++i)
+      uni = off[i + 1] - off[i] == off[1] - off[0] && off[cells + 1 + i] == off[cells + 1];
+    a.uni_units = uni ? off[1] - off[0] : 0;
+    a.uni_nb = uni ? off[cells + 1] : 0;
+  }
   a.n_ctas = n_ctas;
   a.heads_q = static_cast<int>(cfg->heads_q);
   a.n_group = ng;

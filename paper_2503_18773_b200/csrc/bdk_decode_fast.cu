@@ -99,6 +99,15 @@ __device__ __forceinline__ int cta_of_unit(long long u, long long T, int N) {
   return (int)(((u + 1) * (long long)N - 1) / T);
 }
 
+// schedule lookups: arithmetic when every cell has the same units (the host
+// sets uni_units), else the uploaded prefix arrays
+__device__ __forceinline__ long long sched_off(const FastArgs& a, int cell) {
+  return a.uni_units ? (long long)cell * a.uni_units : (long long)__ldg(a.unit_off + cell);
+}
+__device__ __forceinline__ int sched_nb(const FastArgs& a, int cell) {
+  return a.uni_units ? a.uni_nb : __ldg(a.unit_nb + cell);
+}
+
 __device__ __forceinline__ int find_cell(const int* off, int cells, long long u) {
   int lo = 0, hi = cells - 1;  // largest c with off[c] <= u
   while (lo < hi) {
@@ -466,10 +475,10 @@ __device__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& p
   int it = 0;
   long long u = px.u_begin;
   for (int cell = px.cell0; u < px.u_end; ++cell) {
-    const long long ce = __ldg(a.unit_off + cell + 1);
+    const long long ce = sched_off(a, cell + 1);
     const long long seg_end = min(px.u_end, ce);
     const long long pk_end =
-        min(seg_end, (long long)__ldg(a.unit_off + cell) + __ldg(a.unit_nb + cell));
+        min(seg_end, sched_off(a, cell) + sched_nb(a, cell));
     if (u < pk_end) {
       const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
       uint32_t q2[H2];
@@ -818,7 +827,8 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   // this one is resident (the grid is one wave, so this cannot starve it)
   pdl_launch_dependents();
   if (u_begin >= u_end) return;
-  const int cell0 = find_cell(a.unit_off, cells, u_begin);
+  const int cell0 =
+      a.uni_units ? (int)(u_begin / a.uni_units) : find_cell(a.unit_off, cells, u_begin);
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * 16 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
 
@@ -837,9 +847,9 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
         waited = true;
       }
       for (int cell = cell0; u < u_end; ++cell) {
-        const long long cb = __ldg(a.unit_off + cell), ce = __ldg(a.unit_off + cell + 1);
+        const long long cb = sched_off(a, cell), ce = sched_off(a, cell + 1);
         const long long seg_end = min(u_end, ce);
-        const long long pk_end = min(seg_end, cb + (long long)__ldg(a.unit_nb + cell));
+        const long long pk_end = min(seg_end, cb + (long long)sched_nb(a, cell));
         const uint8_t* base = c.records + (size_t)cell * G.max_blocks * REC;
         for (long long x = u; x < pk_end; ++x, ++it) {
           const int s = it % NS;
@@ -898,9 +908,9 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   int it = 0;
   long long u = u_begin;
   for (int cell = cell0; u < u_end; ++cell) {
-    const long long cb = __ldg(a.unit_off + cell), ce = __ldg(a.unit_off + cell + 1);
+    const long long cb = sched_off(a, cell), ce = sched_off(a, cell + 1);
     const long long seg_end = min(u_end, ce);
-    const long long res_begin = cb + (long long)__ldg(a.unit_nb + cell);  // 1st residual unit
+    const long long res_begin = cb + (long long)sched_nb(a, cell);  // 1st residual unit
     const long long pk_end = min(seg_end, res_begin);
     Soft st{-INFINITY, -INFINITY, 0.f, 0.f, 0.f, 0.f};
     float o[OT][4];  // O^T (subnormal-mode scaled, see oscale)

@@ -52,6 +52,7 @@ struct FastArgs {
   const int* unit_nb = nullptr;   // [cells] packed-block units of each cell (the
                                   // rest are residual units of 16*warp_n tokens)
   long long total_units = 0;
+  int uni_units = 0, uni_nb = 0;  // every cell: uni_units units, uni_nb packed (0: use arrays)
   int n_ctas = 0, heads_q = 0, n_group = 0, blk_begin = 0;
   int skip_residual = 0;  // residual units attend nothing (sequence-split ranks)
   float sm_scale_log2 = 0.f;
