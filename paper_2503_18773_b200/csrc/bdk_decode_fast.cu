@@ -74,9 +74,11 @@ struct Smem {
 
 // column packing: with n_group <= 4 an S^T tile only fills accumulator
 // columns 0..3 (heads); the partner tile (same field shifts) is accumulated
-// into columns 4..7 of the same registers, halving the softmax work
+// into columns 4..7 of the same registers, halving the softmax work.  Used
+// at 2-bit (4 tiles per chunk: measured +1% on C2); at 4-bit the two tiles
+// per chunk leave too little to share (measured -3% on C5).
 __host__ __device__ inline int col_pack(const Geom& G, int ng) {
-  return (ng <= 4 && (G.bits == 2 || G.bits == 4)) ? 2 : 1;
+  return (ng <= 4 && G.bits == 2) ? 2 : 1;
 }
 
 __host__ __device__ inline Smem smem_layout(const Geom& G, int ng, int NS, int grp) {
@@ -271,6 +273,29 @@ __device__ __forceinline__ void finalize_segment(Soft st, float (&o)[OT][4], flo
 // turns the pairs of some heads into weights (lanes over contributors,
 // shuffle reductions), (3) each thread owns one float4 of the output in one
 // contributor group and issues MERGE_LB of its loads back to back.
+// s4 += sum over contributors k = kb, kb + step, ... (LB of them, < kc) of
+// w_k * o_k, all LB loads issued back to back
+template <int LB>
+__device__ __forceinline__ float4 merge_batch(const float4* po, int st4, const float* wk, int h,
+                                              int kb, int step, int kc, float4 s4) {
+  float4 o[LB];
+#pragma unroll
+  for (int i = 0; i < LB; ++i) {
+    const int k = kb + i * step;
+    o[i] = k < kc ? __ldcg(po + (size_t)k * st4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < LB; ++i) {
+    const int k = kb + i * step;
+    const float w = k < kc ? wk[k * 8 + h] : 0.f;
+    s4.x = fmaf(o[i].x, w, s4.x);
+    s4.y = fmaf(o[i].y, w, s4.y);
+    s4.z = fmaf(o[i].z, w, s4.z);
+    s4.w = fmaf(o[i].w, w, s4.w);
+  }
+  return s4;
+}
+
 template <int NC>
 __device__ void merge_cell(const FastArgs& a, const Geom& G, int cell, const float* base, int nk,
                            float* sm, unsigned long long* tr) {
@@ -345,23 +370,12 @@ __device__ void merge_cell(const FastArgs& a, const Geom& G, int cell, const flo
         const float r = rsh[h];
         float4 s4 = make_float4(acc[v].x * r, acc[v].y * r, acc[v].z * r, acc[v].w * r);
         const float4* po = reinterpret_cast<const float4*>(base + (size_t)k0 * stride) + e;
-        for (int kb = grp; kb < kc; kb += MERGE_LB * ngrp) {
-          float4 o[MERGE_LB];
-#pragma unroll
-          for (int i = 0; i < MERGE_LB; ++i) {
-            const int k = kb + i * ngrp;
-            o[i] = k < kc ? __ldcg(po + (size_t)k * st4) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-#pragma unroll
-          for (int i = 0; i < MERGE_LB; ++i) {
-            const int k = kb + i * ngrp;
-            const float w = k < kc ? wk[k * 8 + h] : 0.f;
-            s4.x = fmaf(o[i].x, w, s4.x);
-            s4.y = fmaf(o[i].y, w, s4.y);
-            s4.z = fmaf(o[i].z, w, s4.z);
-            s4.w = fmaf(o[i].w, w, s4.w);
-          }
-        }
+        // few contributors (the usual case): a short batch; else deep batches
+        if (kc <= 8 * ngrp)
+          s4 = merge_batch<8>(po, st4, wk, h, grp, ngrp, kc, s4);
+        else
+          for (int kb = grp; kb < kc; kb += MERGE_LB * ngrp)
+            s4 = merge_batch<MERGE_LB>(po, st4, wk, h, kb, ngrp, kc, s4);
         acc[v] = s4;
       }
     }
@@ -563,7 +577,7 @@ __device__ __forceinline__ void consume_block(const uint8_t* rec, const uint8_t*
   float chn[NCH][4];
 #pragma unroll
   for (int i = 0; i < NCH; ++i) chn[i][0] = chn[i][1] = chn[i][2] = chn[i][3] = 0.f;
-  if (!(dev_flags & 4)) {  // dev probe 4: skip the K side
+  {
     const uint32_t kw = smem_u32(rec);
     uint32_t kr[4][4];
 #pragma unroll
@@ -669,7 +683,6 @@ __device__ __forceinline__ void consume_block(const uint8_t* rec, const uint8_t*
     if (lane == 0) mbar_arrive(empty_s);  // ring slot + prep slot are free
 #pragma unroll
     for (int mt = 0; mt < KT; ++mt) {
-      if (dev_flags & 8) break;  // dev probe 8: skip the V side
       const uint32_t ra = vr[mt / 2][2 * (mt % 2)], rb = vr[mt / 2][2 * (mt % 2) + 1];
       const uint32_t ra8 = ra >> 8, rb8 = rb >> 8;
 #pragma unroll
