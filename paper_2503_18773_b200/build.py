@@ -19,7 +19,7 @@ SOURCES = ["bdk_kernels.cu", "bdk_decode_fast.cu", "bdk_api.cu"]
 HEADERS = ["bdk_common.cuh", "bdk_frag.cuh", "bdk_qpack.cuh", "bdk_qpack_fast.cuh", "bdk_launch.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-diag-suppress", "177", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-cudart", "static"]
 
 

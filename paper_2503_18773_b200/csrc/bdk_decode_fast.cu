@@ -59,10 +59,7 @@ struct FC {
   static constexpr int P = 16 / BITS;
   static constexpr int NPAIR = P / 2;          // S^T m16 tiles per chunk (P >= 2)
   static constexpr int RB = 16 * WN;           // bytes per channel row
-  static constexpr int GRP = GRP_;             // consumer groups (alternate blocks)
-  static constexpr int NC = WN * GRP;          // consumer warps
-  static constexpr int NT = (NC + 1 + GRP) * 32;  // + TMA warp + one prep warp per group
-  static constexpr int MINB = MINB_;
+  static constexpr int NC = WN * GRP_;         // consumer warps (+ TMA warp + GRP_ prep warps)
 };
 
 struct Smem {
@@ -273,6 +270,105 @@ __device__ __forceinline__ void finalize_segment(Soft st, float (&o)[OT][4], flo
 // turns the pairs of some heads into weights (lanes over contributors,
 // shuffle reductions), (3) each thread owns one float4 of the output in one
 // contributor group and issues MERGE_LB of its loads back to back.
+constexpr int MERGE_KC_FEW = 16;
+
+// LSE merge for few contributors (<= MERGE_KC_FEW, the batched-decode case):
+// one round of (max, sum) loads into shared memory, weights by one thread
+// per head, then every thread owns float4s of the output and issues the
+// chunk's loads back to back.  Measured faster than merge_cell below when a
+// cell has a handful of partials (C2: +2%), slower for tens (C5: -3%).
+template <int NC>
+__device__ void merge_cell_few(const FastArgs& a, const Geom& G, int cell, const float* base, int nk,
+                           float* sm, unsigned long long* tr) {
+  constexpr int NTH = NC * 32;
+  constexpr int NV = (8 * D / 4 + NTH - 1) / NTH;  // float4 outputs per thread (max)
+  const int ng = a.n_group;
+  const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
+  const int stride = slot_stride(ng);
+  float* msh = sm;        // [8] running max per head
+  float* lsh = sm + 8;    // [8] running sum per head
+  float* rsh = sm + 16;   // [8] rescale of the previous chunks
+  float* wk = sm + 24;    // [MERGE_KC_FEW][8] weights
+  float* lk = wk + MERGE_KC_FEW * 8;  // [MERGE_KC_FEW][8] sums
+  const int nvec = ng * D / 4;
+  float4 acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x < 8) {
+    msh[threadIdx.x] = -INFINITY;
+    lsh[threadIdx.x] = 0.f;
+  }
+  for (int k0 = 0; k0 < nk; k0 += MERGE_KC_FEW) {
+    const int kc = min(MERGE_KC_FEW, nk - k0);
+    for (int idx = threadIdx.x; idx < kc * ng; idx += NTH) {
+      const int k = idx / ng, h = idx % ng;
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(
+          base + (size_t)(k0 + k) * stride + ng * D + 2 * h));
+      wk[k * 8 + h] = ml.x;
+      lk[k * 8 + h] = ml.y;
+    }
+    named_bar(1, NTH);
+    if (threadIdx.x < ng) {
+      const int h = threadIdx.x;
+      const float mo = msh[h];
+      float mx = mo;
+      for (int k = 0; k < kc; ++k) mx = fmaxf(mx, wk[k * 8 + h]);
+      const float r = mo == -INFINITY ? 0.f : ex2(mo - mx);
+      float l = lsh[h] * r;
+      for (int k = 0; k < kc; ++k) {
+        const float m = wk[k * 8 + h];
+        const float w = m == -INFINITY ? 0.f : ex2(m - mx);
+        wk[k * 8 + h] = w;
+        l = fmaf(lk[k * 8 + h], w, l);
+      }
+      lsh[h] = l;
+      msh[h] = mx;
+      rsh[h] = r;
+    }
+    named_bar(1, NTH);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int e = threadIdx.x + v * NTH;
+      if (e < nvec) {
+        const int h = (4 * e) / D;
+        const float r = rsh[h];
+        float4 s4 = make_float4(acc[v].x * r, acc[v].y * r, acc[v].z * r, acc[v].w * r);
+        const float4* po = reinterpret_cast<const float4*>(base + (size_t)k0 * stride) + e;
+        const int st4 = stride / 4;
+        float4 o[MERGE_KC_FEW];
+#pragma unroll
+        for (int k = 0; k < MERGE_KC_FEW; ++k)
+          o[k] = k < kc ? __ldcg(po + (size_t)k * st4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < MERGE_KC_FEW; ++k) {
+          const float w = k < kc ? wk[k * 8 + h] : 0.f;
+          s4.x = fmaf(o[k].x, w, s4.x);
+          s4.y = fmaf(o[k].y, w, s4.y);
+          s4.z = fmaf(o[k].z, w, s4.z);
+          s4.w = fmaf(o[k].w, w, s4.w);
+        }
+        acc[v] = s4;
+      }
+    }
+    named_bar(1, NTH);  // wk / lk reused by the next chunk
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int e = threadIdx.x + v * NTH;
+    if (e < nvec) {
+      const int h = (4 * e) / D, ch = (4 * e) % D;
+      const float l = lsh[h];
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const size_t row = (size_t)bidx * a.heads_q + (size_t)hk * ng + h;
+      const float4 s4 = acc[v];
+      *reinterpret_cast<float4*>(a.out + row * D + ch) =
+          make_float4(s4.x * inv, s4.y * inv, s4.z * inv, s4.w * inv);
+      if (a.out_lse != nullptr && ch == 0)
+        a.out_lse[row] = l > 0.f ? msh[h] + __log2f(l) : -INFINITY;
+    }
+  }
+}
+
 // s4 += sum over contributors k = kb, kb + step, ... (LB of them, < kc) of
 // w_k * o_k, all LB loads issued back to back
 template <int LB>
@@ -485,7 +581,6 @@ __device__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& p
   const int lane = threadIdx.x & 31;
   const int h = lane % NH, cbk = lane / NH;
   const int ng = a.n_group;
-  const int gpb = G.k_axis == 0 ? G.n_r / G.g : 1;
   int it = 0;
   long long u = px.u_begin;
   for (int cell = px.cell0; u < px.u_end; ++cell) {
@@ -794,7 +889,7 @@ template <int BITS, int WN, int NS, int MINB, int GRP, int CP>
 __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     decode_fast_kernel(DevCache c, FastArgs a) {
   using C = FC<BITS, WN, MINB, GRP>;
-  constexpr int P = C::P, NPAIR = C::NPAIR, NC = C::NC, RB = C::RB;
+  constexpr int P = C::P, NPAIR = C::NPAIR, NC = C::NC;
   static_assert(CP == 1 || (CP == 2 && NPAIR % 2 == 0), "column packing pairs tiles");
   constexpr int NPK = NPAIR / CP;  // packed S^T accumulators per chunk
   static_assert(NS % GRP == 0, "stage s must always belong to consumer group s % GRP");
@@ -815,7 +910,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   uint64_t* ready = empty + NS;
   int* flag = reinterpret_cast<int*>(ready + NS);
   int* claim = flag + 2;  // [WN] next block per chunk position (GRP > 1)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, t4 = lane & 3;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t4 = lane & 3;
   const int REC = G.rec_bytes;
 
   // zero the prep areas once: Q' rows of heads >= n_group stay zero
@@ -1003,9 +1098,13 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     }
     named_bar(1, NC * 32);
     if (tr && threadIdx.x == 0) tr[10] = globaltimer();
-    if (*flag)
-      merge_cell<NC>(a, G, cell, a.slots + (size_t)(lo + cell) * stride_slot, hi - lo + 1, merge_sm,
-                     tr);
+    if (*flag) {
+      const float* base = a.slots + (size_t)(lo + cell) * stride_slot;
+      if (hi - lo + 1 <= MERGE_KC_FEW)
+        merge_cell_few<NC>(a, G, cell, base, hi - lo + 1, merge_sm, tr);
+      else
+        merge_cell<NC>(a, G, cell, base, hi - lo + 1, merge_sm, tr);
+    }
     if (tr && threadIdx.x == 0) {
       tr[5] = globaltimer();
       tr[6] = (unsigned long long)(*flag);
