@@ -201,6 +201,22 @@ BDK_API bdk_status bdk_dequant_blocks(const bdk_cache* cache, uint32_t b, uint32
 /* KVCache::memory (kvcache.cpp:330-345): {k payload, v payload, params,
  * residual} bytes. */
 BDK_API bdk_status bdk_memory(const bdk_cache* cache, uint64_t out[4]);
+
+/* ------------------------------------------------ BDKV v1 cache files */
+/* dump_cache / load_cache (serialize.hpp:11-23, serialize.cpp:87-194): the
+ * reference's byte format.  bdk_dump_cache writes into buf (capacity bytes)
+ * and sets *size; buf == NULL queries the size.  bdk_load_cache builds a new
+ * cache (contiguous backend) with max(max_tokens, longest cell + N_r) token
+ * capacity; bad magic / version / fields or truncation -> BDK_FORMAT_ERROR
+ * with the byte offset in bdk_last_error(). */
+BDK_API bdk_status bdk_dump_cache(const bdk_cache* cache, uint8_t* buf, uint64_t capacity,
+                                  uint64_t* size);
+BDK_API bdk_status bdk_load_cache(const uint8_t* buf, uint64_t size, uint32_t max_tokens,
+                                  int32_t device, bdk_cache** out);
+/* dump_cache_file / load_cache_file (serialize.hpp:22-23) */
+BDK_API bdk_status bdk_dump_cache_file(const bdk_cache* cache, const char* path);
+BDK_API bdk_status bdk_load_cache_file(const char* path, uint32_t max_tokens, int32_t device,
+                                       bdk_cache** out);
 /* KVCache::corrupt_word (kvcache.cpp:326-328): fault injection on K words. */
 BDK_API bdk_status bdk_corrupt_word(bdk_cache* cache, uint32_t b, uint32_t h, uint32_t blk,
                                     uint32_t word, uint16_t value);

@@ -21,7 +21,11 @@
 #include <utility>
 #include <cstddef>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <istream>
+#include <iterator>
+#include <ostream>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -54,8 +58,15 @@ struct CapacityError : Error {
 struct StateError : Error {
   using Error::Error;
 };
-struct FormatError : Error {
-  using Error::Error;
+struct FormatError : Error {  // errors.hpp: carries the byte offset
+  explicit FormatError(const std::string& m) : Error(m), offset(parse_offset(m)) {}
+  size_t offset;
+
+ private:
+  static size_t parse_offset(const std::string& m) {
+    const auto p = m.rfind("byte offset ");
+    return p == std::string::npos ? 0 : static_cast<size_t>(std::stoull(m.substr(p + 12)));
+  }
 };
 struct EmptyInput : Error {
   using Error::Error;
@@ -403,8 +414,28 @@ class KVCache {  // kvcache.hpp:103-189, cache resident in HBM
   // fp16 P (false, default) or the hi/lo split PV with bit-faithful dequant
   // (true): the reference's own 1e-5 tolerances
   void set_precise(bool precise) { detail::check(bdk_set_precise(h_, precise ? 1 : 0)); }
+  // empty every cell, keeping the device arena (a fresh KVCache of the same
+  // geometry without reallocating)
+  void reset() { detail::check(bdk_cache_reset(h_, nullptr)); }
+
+  // adopt a handle the C-ABI created (load_cache); geometry from the BDKV
+  // header fields (serialize.hpp:11-20)
+  static KVCache adopt(bdk_cache* h, uint32_t bits, uint32_t axis, uint32_t g, uint32_t n_r,
+                       uint32_t d, uint32_t batch, uint32_t heads, bool interleave) {
+    KVCache c;
+    c.h_ = h;
+    c.batch_ = batch;
+    c.heads_kv_ = heads;
+    c.head_dim_ = d;
+    c.warp_n_ = n_r / (8 * (16 / bits));
+    c.spec_ = QuantSpec{bits, static_cast<QuantAxis>(axis), g};
+    c.interleave_ = interleave;
+    detail::check(bdk_cache_get_info(h, &c.info_));
+    return c;
+  }
 
  private:
+  KVCache() = default;
   std::pair<size_t, size_t> lengths(size_t b, size_t h) const {
     uint32_t p = 0, r = 0;
     detail::check(bdk_cache_lengths(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h), &p,
@@ -450,6 +481,51 @@ inline AttnOutput decode_step(KVCache& cache, const AttentionConfig& cfg, const 
   detail::check(bdk_decode_step_host(cache.handle(), &c, q.data(), k_new.data(), v_new.data(),
                                      out.data.data()));
   return out;
+}
+
+// ------------------------------------------------------------ serialize.hpp
+// BDKV v1 (serialize.hpp:11-23): the reference's byte format, produced from
+// and loaded into the device cache by the C-ABI (bdk_dump_cache /
+// bdk_load_cache).  max_tokens / device size the loaded cache's arena.
+inline void dump_cache(const KVCache& cache, std::ostream& os) {
+  uint64_t n = 0;
+  detail::check(bdk_dump_cache(cache.handle(), nullptr, 0, &n));
+  std::vector<uint8_t> buf(n);
+  detail::check(bdk_dump_cache(cache.handle(), buf.data(), n, &n));
+  os.write(reinterpret_cast<const char*>(buf.data()), static_cast<std::streamsize>(n));
+  os.flush();
+}
+
+namespace detail {
+inline KVCache adopt_loaded(bdk_cache* h, const std::vector<uint8_t>& hdr) {
+  uint32_t f[7];
+  std::memcpy(f, hdr.data() + 6, sizeof f);  // little-endian host
+  return KVCache::adopt(h, f[0], f[1], f[2], f[3], f[4], f[5], f[6], (hdr[5] & 1) != 0);
+}
+}  // namespace detail
+
+inline KVCache load_cache(std::istream& is, size_t max_tokens = 0, int device = 0) {
+  std::vector<uint8_t> buf((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+  bdk_cache* h = nullptr;
+  detail::check(bdk_load_cache(buf.data(), buf.size(), static_cast<uint32_t>(max_tokens), device,
+                               &h));
+  return detail::adopt_loaded(h, buf);
+}
+
+inline void dump_cache_file(const KVCache& cache, const std::string& path) {
+  detail::check(bdk_dump_cache_file(cache.handle(), path.c_str()));
+}
+
+inline KVCache load_cache_file(const std::string& path, size_t max_tokens = 0, int device = 0) {
+  bdk_cache* h = nullptr;
+  detail::check(bdk_load_cache_file(path.c_str(), static_cast<uint32_t>(max_tokens), device, &h));
+  std::vector<uint8_t> hdr(34, 0);
+  if (FILE* f = std::fopen(path.c_str(), "rb")) {
+    const size_t got = std::fread(hdr.data(), 1, hdr.size(), f);
+    std::fclose(f);
+    (void)got;
+  }
+  return detail::adopt_loaded(h, hdr);
 }
 
 }  // namespace bitkv

@@ -47,6 +47,10 @@ SIGNATURES = {
     "bdk_prefill": (C.c_int, [vp, u32, u32, vp, vp, u32, vp]),
     "bdk_prefill_all": (C.c_int, [vp, vp, vp, u32, vp]),
     "bdk_cache_reset": (C.c_int, [vp, vp]),
+    "bdk_dump_cache": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(C.c_uint64)]),
+    "bdk_load_cache": (C.c_int, [vp, C.c_uint64, u32, C.c_int32, C.POINTER(vp)]),
+    "bdk_dump_cache_file": (C.c_int, [vp, C.c_char_p]),
+    "bdk_load_cache_file": (C.c_int, [C.c_char_p, u32, C.c_int32, C.POINTER(vp)]),
     "bdk_prefill_host": (C.c_int, [vp, u32, u32, u16p, u16p, u32]),
     "bdk_append_token_host": (C.c_int, [vp, u32, u32, u16p, u16p]),
     "bdk_packed_tile_host": (C.c_int, [vp, u32, u32, u32, u32, u16p, u16p]),

@@ -59,7 +59,13 @@ class StateError(Error):
 
 
 class FormatError(Error):
-    pass
+    """bitkv::FormatError (errors.hpp); ``offset`` is the byte offset."""
+
+    @property
+    def offset(self) -> int | None:
+        import re
+        m = re.search(r"byte offset (\d+)", str(self))
+        return int(m.group(1)) if m else None
 
 
 class EmptyInput(Error):
@@ -224,6 +230,25 @@ class KVCache:
         info = _L.CacheInfo()
         _check(_L.load().bdk_cache_get_info(self._h, C.byref(info)))
         self.info = info
+
+    @classmethod
+    def _adopt(cls, handle, header: bytes, device: int) -> "KVCache":
+        """Wrap a cache the C-ABI created (load_cache); geometry from the
+        BDKV header (serialize.hpp:11-20)."""
+        import struct
+        flags = header[5]
+        bits, axis, g, n_r, d, batch, heads = struct.unpack_from("<7I", header, 6)
+        self = cls.__new__(cls)
+        self._h = handle
+        self._batch, self._heads_kv, self._d = batch, heads, d
+        self._warp_n = n_r // (8 * (16 // bits))
+        self._spec = QuantSpec(bits, QuantAxis(axis), g)
+        self._interleave, self._device = bool(flags & 1), device
+        self._backend, self._page_size = CacheBackend.Contiguous, 16
+        info = _L.CacheInfo()
+        _check(_L.load().bdk_cache_get_info(self._h, C.byref(info)))
+        self.info = info
+        return self
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -410,6 +435,41 @@ class AttnOutput:
 
     def row(self, b: int, h: int):
         return self.data[b, h]
+
+
+# ------------------------------------------------------------- serialize.hpp
+def dump_cache(cache: KVCache) -> bytes:
+    """dump_cache (serialize.hpp:19, serialize.cpp:87-122): BDKV v1 bytes."""
+    n = C.c_uint64()
+    L = _L.load()
+    _check(L.bdk_dump_cache(cache.handle(), None, 0, C.byref(n)))
+    buf = (C.c_uint8 * n.value)()
+    _check(L.bdk_dump_cache(cache.handle(), buf, n.value, C.byref(n)))
+    return bytes(buf)
+
+
+def load_cache(data: bytes, *, max_tokens: int = 0, device: int = 0) -> KVCache:
+    """load_cache (serialize.hpp:20, serialize.cpp:124-194); always a
+    contiguous backend.  The arena holds max(max_tokens, longest cell + N_r)."""
+    data = bytes(data)
+    h = C.c_void_p()
+    buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+    _check(_L.load().bdk_load_cache(buf, len(data), max_tokens, device, C.byref(h)))
+    return KVCache._adopt(h, data[:34], device)
+
+
+def dump_cache_file(cache: KVCache, path: str) -> None:
+    """dump_cache_file (serialize.hpp:22)."""
+    _check(_L.load().bdk_dump_cache_file(cache.handle(), str(path).encode()))
+
+
+def load_cache_file(path: str, *, max_tokens: int = 0, device: int = 0) -> KVCache:
+    """load_cache_file (serialize.hpp:23)."""
+    h = C.c_void_p()
+    _check(_L.load().bdk_load_cache_file(str(path).encode(), max_tokens, device, C.byref(h)))
+    with open(path, "rb") as f:
+        header = f.read(34)
+    return KVCache._adopt(h, header, device)
 
 
 def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None) -> AttnOutput:

@@ -950,4 +950,271 @@ bdk_status bdk_synchronize(void) {
   return BDK_OK;
 }
 
+
+// ------------------------------------------------------------- BDKV v1
+// The reference's on-disk cache format (serialize.hpp:11-20,
+// serialize.cpp:87-194), all integers little-endian:
+//   "BDKV" | version u8 (1) | flags u8 (bit0 = interleaved layout)
+//   u32 num_bits, k_axis, group_size, N_r, head_dim, batch, heads_kv
+//   per cell (batch-major): u32 packed_len, u32 res_len, then the K words of
+//   every block, the K params of every block, the V words, the V params
+//   (u16 arrays in block order), then res_len*d residual K binary16 bits and
+//   the same for V.
+// The device records hold the same words (only chunk-swizzled) and the same
+// (scale, zero) u16 pairs, so a dump is a per-cell D2H copy plus the
+// un-swizzle, and a load the reverse.  FormatError messages carry the byte
+// offset like the reference's FormatError::offset.
+namespace {
+
+void put_u32(std::vector<uint8_t>& o, uint32_t v) {
+  for (int i = 0; i < 4; ++i) o.push_back(static_cast<uint8_t>(v >> (8 * i)));
+}
+
+bdk_status format_fail(const std::string& what, uint64_t offset) {
+  return fail(BDK_FORMAT_ERROR, what + " (at byte offset " + std::to_string(offset) + ")");
+}
+
+struct BdkvReader {
+  const uint8_t* p;
+  uint64_t n, off = 0;
+  bool u8(uint8_t& v) {
+    if (off + 1 > n) return false;
+    v = p[off++];
+    return true;
+  }
+  bool u32(uint32_t& v) {
+    if (off + 4 > n) return false;
+    v = (uint32_t)p[off] | (uint32_t)p[off + 1] << 8 | (uint32_t)p[off + 2] << 16 |
+        (uint32_t)p[off + 3] << 24;
+    off += 4;
+    return true;
+  }
+  bool skip(uint64_t bytes) {
+    if (bytes > n - off) return false;
+    off += bytes;
+    return true;
+  }
+};
+
+bdk_status serialize(const bdk_cache* c, std::vector<uint8_t>& o) {
+  const Geom& G = c->dev.G;
+  const uint32_t d = c->desc.head_dim;
+  o.clear();
+  const char magic[4] = {'B', 'D', 'K', 'V'};
+  o.insert(o.end(), magic, magic + 4);
+  o.push_back(1);
+  o.push_back(c->desc.interleave ? 1 : 0);
+  put_u32(o, c->desc.num_bits);
+  put_u32(o, c->desc.k_axis);
+  put_u32(o, c->desc.group_size);
+  put_u32(o, (uint32_t)G.n_r);
+  put_u32(o, d);
+  put_u32(o, c->desc.batch);
+  put_u32(o, c->desc.heads_kv);
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(cudaDeviceSynchronize(), "sync");
+  std::vector<uint8_t> recs;
+  std::vector<uint16_t> res;
+  const size_t cells = c->res_len.size();
+  for (size_t i = 0; i < cells; ++i) {
+    const uint32_t nb = (uint32_t)c->packed_blocks[i], rl = (uint32_t)c->res_len[i];
+    put_u32(o, nb * (uint32_t)G.n_r);
+    put_u32(o, rl);
+    recs.resize((size_t)nb * G.rec_bytes);
+    if (nb)
+      BDK_CUDA(cudaMemcpy(recs.data(), c->dev.records + (size_t)i * G.max_blocks * G.rec_bytes,
+                          recs.size(), cudaMemcpyDeviceToHost),
+               "D2H records");
+    // K words | K params | V words | V params, each for every block in order
+    for (int part = 0; part < 4; ++part) {
+      for (uint32_t blk = 0; blk < nb; ++blk) {
+        const uint8_t* rec = recs.data() + (size_t)blk * G.rec_bytes;
+        if (part == 0 || part == 2) {
+          const uint8_t* words = rec + (part == 2 ? G.wbytes : 0);
+          for (uint32_t w = 0; w < c->wpb; ++w) {
+            const uint8_t* src = words + word_offset(G, w);
+            o.push_back(src[0]);
+            o.push_back(src[1]);
+          }
+        } else {
+          const uint8_t* prm = rec + 2 * G.wbytes + (part == 3 ? G.kp_bytes : 0);
+          const uint32_t nbytes = 2 * (part == 1 ? c->kp_u16 : c->vp_u16);
+          o.insert(o.end(), prm, prm + nbytes);
+        }
+      }
+    }
+    res.resize((size_t)rl * d);
+    for (int t = 0; t < 2; ++t) {
+      if (rl)
+        BDK_CUDA(cudaMemcpy(res.data(), (t ? c->dev.res_v : c->dev.res_k) + i * (size_t)G.n_r * d,
+                            res.size() * 2, cudaMemcpyDeviceToHost),
+                 "D2H residual");
+      for (uint16_t x : res) {
+        o.push_back(static_cast<uint8_t>(x & 0xFF));
+        o.push_back(static_cast<uint8_t>(x >> 8));
+      }
+    }
+  }
+  return BDK_OK;
+}
+
+}  // namespace
+
+bdk_status bdk_dump_cache(const bdk_cache* c, uint8_t* buf, uint64_t capacity, uint64_t* size) {
+  if (!c || !size) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  std::vector<uint8_t> o;
+  bdk_status s = serialize(c, o);
+  if (s) return s;
+  *size = o.size();
+  if (!buf) return BDK_OK;
+  if (capacity < o.size())
+    return fail(BDK_CAPACITY_ERROR, "dump buffer too small: need " + std::to_string(o.size()));
+  std::memcpy(buf, o.data(), o.size());
+  return BDK_OK;
+}
+
+bdk_status bdk_dump_cache_file(const bdk_cache* c, const char* path) {
+  if (!c || !path) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  std::vector<uint8_t> o;
+  bdk_status s = serialize(c, o);
+  if (s) return s;
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(BDK_INVALID_ARGUMENT, std::string("cannot open ") + path + " for writing");
+  const bool ok = std::fwrite(o.data(), 1, o.size(), f) == o.size();
+  if (std::fclose(f) != 0 || !ok)
+    return fail(BDK_INVALID_ARGUMENT, std::string("write to ") + path + " failed");
+  return BDK_OK;
+}
+
+bdk_status bdk_load_cache(const uint8_t* buf, uint64_t size, uint32_t max_tokens, int32_t device,
+                          bdk_cache** out) {
+  if (!out || (!buf && size)) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  BdkvReader r{buf, size};
+  const auto eof = [&]() { return format_fail("unexpected end of file", r.n); };
+  if (size < 4) return format_fail("unexpected end of file", size);
+  if (std::memcmp(buf, "BDKV", 4) != 0) return format_fail("bad magic", 0);
+  r.off = 4;
+  uint8_t version = 0, flags = 0;
+  if (!r.u8(version)) return eof();
+  if (version != 1) return format_fail("unsupported version " + std::to_string(version), 4);
+  if (!r.u8(flags)) return eof();
+  uint32_t bits, axis, g, n_r, d, batch, heads;
+  if (!r.u32(bits)) return eof();
+  if (!r.u32(axis)) return eof();
+  if (axis > 1) return format_fail("bad quant axis", r.off - 4);
+  if (!r.u32(g) || !r.u32(n_r) || !r.u32(d) || !r.u32(batch) || !r.u32(heads)) return eof();
+  if (bits == 0 || bits > 16 || n_r == 0 || n_r % (8 * (16 / bits)) != 0)
+    return format_fail("N_r inconsistent with num_bits", 10);
+  const uint32_t warp_n = n_r / (8 * (16 / bits));
+  // pass 1: validate every cell and size the arena
+  const uint64_t wpb = (uint64_t)n_r * d * bits / 16;
+  const bool pass = bits == 16;
+  const uint64_t kp = pass ? 0
+                      : 2ull * (axis == 0 ? (uint64_t)(g ? n_r / g : 0) * d
+                                          : (uint64_t)n_r * (g ? d / g : 0));
+  const uint64_t vp = pass ? 0 : 2ull * n_r * (g ? d / g : 0);
+  const uint64_t body = r.off;
+  uint64_t need = 0;
+  const uint64_t cells = (uint64_t)batch * heads;
+  for (uint64_t i = 0; i < cells; ++i) {
+    uint32_t plen, rlen;
+    if (!r.u32(plen) || !r.u32(rlen)) return eof();
+    if (plen % n_r != 0) return format_fail("packed_len not block-aligned", r.off - 8);
+    if (rlen >= n_r) return format_fail("res_len must be < N_r", r.off - 4);
+    const uint64_t blocks = plen / n_r;
+    if (!r.skip(2 * blocks * (2 * wpb + kp + vp) + 4ull * rlen * d))
+      return format_fail("unexpected end of file", r.n);
+    need = std::max<uint64_t>(need, (uint64_t)plen + rlen);
+  }
+  bdk_cache_desc desc{};
+  desc.batch = batch;
+  desc.heads_kv = heads;
+  desc.head_dim = d;
+  desc.warp_n = warp_n;
+  desc.num_bits = bits;
+  desc.k_axis = axis;
+  desc.group_size = g;
+  desc.interleave = flags & 1;
+  desc.max_tokens = (uint32_t)std::max<uint64_t>(max_tokens, need + n_r);
+  desc.device = device;
+  bdk_cache* c = nullptr;
+  bdk_status s = bdk_cache_create(&desc, &c);
+  if (s) return s;
+  const Geom& G = c->dev.G;
+  if (c->wpb != wpb || c->kp_u16 != kp || c->vp_u16 != vp) {  // cannot happen for valid geometry
+    bdk_cache_destroy(c);
+    return format_fail("array sizes inconsistent with the header", 6);
+  }
+  // pass 2: fill the device arena
+  r.off = body;
+  std::vector<uint8_t> recs;
+  std::vector<int> nbs(cells), rls(cells);
+  for (uint64_t i = 0; i < cells; ++i) {
+    uint32_t plen, rlen;
+    r.u32(plen);
+    r.u32(rlen);
+    const uint32_t nb = plen / n_r;
+    recs.assign((size_t)nb * G.rec_bytes, 0);
+    for (int part = 0; part < 4; ++part) {
+      for (uint32_t blk = 0; blk < nb; ++blk) {
+        uint8_t* rec = recs.data() + (size_t)blk * G.rec_bytes;
+        if (part == 0 || part == 2) {
+          uint8_t* words = rec + (part == 2 ? G.wbytes : 0);
+          for (uint32_t w = 0; w < wpb; ++w) {
+            std::memcpy(words + word_offset(G, w), buf + r.off, 2);
+            r.off += 2;
+          }
+        } else {
+          const uint64_t nbytes = 2 * (part == 1 ? kp : vp);
+          std::memcpy(rec + 2 * G.wbytes + (part == 3 ? G.kp_bytes : 0), buf + r.off, nbytes);
+          r.off += nbytes;
+        }
+      }
+    }
+    cudaError_t e = cudaSuccess;
+    if (nb)
+      e = cudaMemcpy(c->dev.records + (size_t)i * G.max_blocks * G.rec_bytes, recs.data(),
+                     recs.size(), cudaMemcpyHostToDevice);
+    for (int t = 0; t < 2 && e == cudaSuccess; ++t) {
+      if (rlen)
+        e = cudaMemcpy((t ? c->dev.res_v : c->dev.res_k) + i * (size_t)G.n_r * d, buf + r.off,
+                       (size_t)rlen * d * 2, cudaMemcpyHostToDevice);
+      r.off += (uint64_t)rlen * d * 2;
+    }
+    if (e != cudaSuccess) {
+      bdk_cache_destroy(c);
+      return cuda_fail(e, "H2D load");
+    }
+    nbs[i] = (int)nb;
+    rls[i] = (int)rlen;
+  }
+  cudaError_t e = cudaMemcpy(c->dev.packed_blocks, nbs.data(), cells * sizeof(int),
+                             cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(c->dev.res_len, rls.data(), cells * sizeof(int), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    bdk_cache_destroy(c);
+    return cuda_fail(e, "H2D lengths");
+  }
+  c->packed_blocks = nbs;
+  c->res_len = rls;
+  c->blocks_written = true;
+  *out = c;
+  return BDK_OK;
+}
+
+bdk_status bdk_load_cache_file(const char* path, uint32_t max_tokens, int32_t device,
+                               bdk_cache** out) {
+  if (!path || !out) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  FILE* f = std::fopen(path, "rb");
+  if (!f) return fail(BDK_INVALID_ARGUMENT, std::string("cannot open ") + path);
+  std::vector<uint8_t> data;
+  uint8_t chunk[1 << 16];
+  size_t n;
+  while ((n = std::fread(chunk, 1, sizeof(chunk), f)) > 0) data.insert(data.end(), chunk, chunk + n);
+  std::fclose(f);
+  return bdk_load_cache(data.data(), data.size(), max_tokens, device, out);
+}
+
 }  // extern "C"

@@ -6,6 +6,9 @@
 //   run:   needs a B200 (cuda:0); exit code = number of failed checks
 #include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <sstream>
+#include <string>
 #include <vector>
 
 #include "bitkv_b200.hpp"
@@ -162,6 +165,51 @@ static void errors_map_to_reference_exceptions() {
   CHECK(b.k_params.zero(0) == 0.5f && b.k_params.scale(0) == kMinScale);
 }
 
+// test_serialize.cpp:44-82 on the device cache: dump -> load reproduces
+// every cell, re-dump is byte-identical; truncation / bad magic ->
+// FormatError with an offset (:84-104)
+static void serialize_round_trip(uint32_t bits) {
+  const size_t d = 128, n_r = residual_block_size(bits, 4);
+  KVCache cache(2, 2, d, 4, QuantSpec{bits, QuantAxis::KChannel, 128}, CacheBackend::Contiguous,
+                16, 0, true, 4 * n_r);
+  orc_gauss rng;
+  orc_gauss_init(&rng, 500 + bits);
+  for (size_t b = 0; b < 2; ++b)
+    for (size_t h = 0; h < 2; ++h) {
+      const size_t len = n_r + 13 * (b * 2 + h + 1);
+      const auto k = gauss(rng, len * d), v = gauss(rng, len * d);
+      cache.prefill(b, h, k.data(), v.data(), len);
+    }
+  std::ostringstream os(std::ios::binary);
+  dump_cache(cache, os);
+  const std::string bytes = os.str();
+  std::istringstream is(bytes, std::ios::binary);
+  KVCache loaded = load_cache(is);
+  CHECK(loaded.n_r() == cache.n_r() && loaded.batch() == 2 && loaded.heads_kv() == 2);
+  for (size_t b = 0; b < 2; ++b)
+    for (size_t h = 0; h < 2; ++h) {
+      CHECK(loaded.packed_len(b, h) == cache.packed_len(b, h));
+      CHECK(loaded.res_len(b, h) == cache.res_len(b, h));
+      CHECK(loaded.packed(b, h).blocks == cache.packed(b, h).blocks);
+    }
+  std::ostringstream os2(std::ios::binary);
+  dump_cache(loaded, os2);
+  CHECK(os2.str() == bytes);
+  for (size_t cut : {size_t{0}, size_t{3}, size_t{9}, bytes.size() / 2, bytes.size() - 1}) {
+    std::istringstream t(bytes.substr(0, cut), std::ios::binary);
+    CHECK(throws_as<FormatError>([&] { load_cache(t); }));
+  }
+  std::string bad = bytes;
+  bad[0] = 'X';
+  std::istringstream tb(bad, std::ios::binary);
+  try {
+    load_cache(tb);
+    CHECK(false);
+  } catch (const FormatError& e) {
+    CHECK(e.offset == 0);
+  }
+}
+
 int main() {
   prefill_is_bit_exact(4, 4, 128, QuantAxis::KChannel);
   prefill_is_bit_exact(2, 4, 128, QuantAxis::KChannel);
@@ -172,6 +220,8 @@ int main() {
   decode_matches_oracle(true, 4, 32, 8);
   decode_matches_oracle(true, 2, 8, 8);
   errors_map_to_reference_exceptions();
+  serialize_round_trip(4);
+  serialize_round_trip(2);
   std::printf("%s: %d failed checks\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail;
 }

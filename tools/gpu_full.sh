@@ -14,10 +14,19 @@ timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > $O/bench_ref
 timeout 900 python bench.py --impl reference --workload C5 --steps 3 --warmup 1 > $O/bench_ref_C5.json 2> $O/bench_ref_C5.err
 timeout 900 python bench.py --impl reference --workload C4 > $O/bench_ref_C4.json 2> $O/bench_ref_C4.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_C2.csv python bench.py --steps 20 --warmup 3 --soak 0 --e2e-steps 0 --no-cpu-baseline > $O/ncu_launch.log 2>&1
+# full captures: summarized on the box (the .ncu-rep files stay there; the
+# 64 MiB gpurun_out cap would drop everything)
 for w in C2 C5 C3; do
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_fast -s 8 -c 1 -f -o $O/prof_$w python bench.py --workload $w --steps 5 --warmup 3 --soak 0 --e2e-steps 0 --no-cpu-baseline > $O/ncu_full_$w.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_fast -s 8 -c 1 -f -o /tmp/prof_$w python bench.py --workload $w --steps 5 --warmup 3 --soak 0 --e2e-steps 0 --no-cpu-baseline > $O/ncu_full_$w.log 2>&1
+python tools/ncu_summary.py /tmp/prof_$w.ncu-rep > $O/ncu_summary_$w.txt 2>&1
+ncu -i /tmp/prof_$w.ncu-rep --page details --csv > $O/ncu_details_$w.csv 2>/dev/null
+python tools/ncu_mix.py /tmp/prof_$w.ncu-rep > $O/ncu_mix_$w.txt 2>&1
 done
 for w in C4 C4b2; do
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:qpack_fast -s 5 -c 1 -f -o $O/prof_$w python bench.py --workload $w --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $O/ncu_full_$w.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:qpack_fast -s 5 -c 1 -f -o /tmp/prof_$w python bench.py --workload $w --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $O/ncu_full_$w.log 2>&1
+python tools/ncu_summary.py /tmp/prof_$w.ncu-rep > $O/ncu_summary_$w.txt 2>&1
+ncu -i /tmp/prof_$w.ncu-rep --page details --csv > $O/ncu_details_$w.csv 2>/dev/null
+python tools/ncu_mix.py /tmp/prof_$w.ncu-rep > $O/ncu_mix_$w.txt 2>&1
 done
+du -sh $O
 echo done
