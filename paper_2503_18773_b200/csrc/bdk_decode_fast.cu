@@ -1163,8 +1163,9 @@ static int variant_knob() {
 }
 
 // default: two co-resident CTAs per SM, one consumer group each, 4-stage ring
-// (measured best on B200); knob 2 = one CTA per SM with two consumer groups
-// over an 8-stage ring (balanced finish, lower throughput), 3 = three groups.
+// (measured best on B200).  Dev knob BDK_FAST_VARIANT: 2 = one CTA per SM with
+// two consumer groups claiming chunks from a shared 8-stage ring, 3 = three
+// groups at 128 registers (both measured 6-15% slower).
 static Variant fast_kernel(const Geom& G, int ng) {
   const int v = variant_knob();
   static const bool cp_off = getenv("BDK_COLPACK") && atoi(getenv("BDK_COLPACK")) == 0;
@@ -1175,12 +1176,6 @@ static Variant fast_kernel(const Geom& G, int ng) {
     BDK_SEL(2, 4, 8, 1, 2) BDK_SEL(4, 4, 8, 1, 2)
   } else if (v == 3) {
     BDK_SEL(2, 4, 6, 1, 3) BDK_SEL(4, 4, 9, 1, 3)
-  } else if (v == 4) {  // ring depth probes (2 CTAs per SM)
-    BDK_SEL(2, 4, 3, 2, 1) BDK_SEL(4, 4, 3, 2, 1)
-  } else if (v == 5) {
-    BDK_SEL(2, 4, 5, 2, 1) BDK_SEL(4, 4, 5, 2, 1)
-  } else if (v == 6) {
-    BDK_SEL(2, 4, 2, 2, 1) BDK_SEL(4, 4, 2, 2, 1)
   }
   BDK_SEL(2, 1, 4, 2, 1) BDK_SEL(2, 2, 4, 2, 1) BDK_SEL(2, 4, 4, 2, 1) BDK_SEL(2, 8, 4, 1, 1)
   BDK_SEL(4, 1, 4, 2, 1) BDK_SEL(4, 2, 4, 2, 1) BDK_SEL(4, 4, 4, 2, 1) BDK_SEL(4, 8, 4, 1, 1)
