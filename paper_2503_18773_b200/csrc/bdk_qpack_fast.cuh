@@ -14,8 +14,9 @@
 //     zero in scan order, the reference's strict-compare tie rule);
 //   * code = rint((x - z) / s) via x * rcp(s): the product is within 2^-22
 //     relative of the quotient, so it rounds to the same integer unless it
-//     lies within 1e-4 of a half-integer -- those (rare) elements take the
-//     exact IEEE division (__fdiv_rn), so every code equals the reference's;
+//     lies within 4 * 2^-22 * 2^BITS of a half-integer -- those elements
+//     (exact .5 quotients are common on fp16 grids) take the exact IEEE
+//     division (__fdiv_rn), so every code equals the reference's;
 //   * the params are assembled in shared memory and written with one TMA
 //     bulk store; the words go out as 16-byte stores in the record's
 //     (swizzled) row layout.
@@ -81,7 +82,7 @@ __device__ __noinline__ uint32_t exact_word(const __half* tile, const float4* fs
 // is one 128-token group).  Codes need no clamp here: z = lo exactly and
 // s >= (hi - lo) / qmax * (1 - 2^-11), so every in-group quotient lies in
 // [0, qmax + 0.5).
-template <int BITS, bool TOKEN_PARAMS>
+template <int BITS, bool TOKEN_PARAMS, bool IL>
 __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, uint8_t* words,
                                         const Geom& G, int hf) {
   constexpr int P = 16 / BITS;
@@ -92,9 +93,14 @@ __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, ui
   constexpr int NP = 4 / SPLIT;  // u32 word pairs per item
   const __half2* tile2 = reinterpret_cast<const __half2*>(tile);
   const int wn = G.warp_n, rb = 16 * wn;
+  // IL: the token order is a compile-time constant, so every tile offset
+  // below folds into the load's immediate
   int tok[P];
 #pragma unroll
-  for (int p = 0; p < P; ++p) tok[p] = pos_token(p, P, G.interleave);
+  for (int p = 0; p < P; ++p) tok[p] = pos_token(p, P, IL ? 1 : 0);
+  // |q - x/s| <= 2^-22 q: a product farther than 4 * 2^-22 * (qmax + 1) from a
+  // half-integer rounds like the exact quotient
+  constexpr float TIE = 0.5f - 4.f * (1.f / 4194304.f) * (float)(1 << BITS);
   for (int item = threadIdx.x; item < SPLIT * CPT * (QF_D / 2); item += QF_THREADS) {
     const int sp = item / (CPT * (QF_D / 2));
     const int jl = (item / (QF_D / 2)) % CPT, cp = item % (QF_D / 2);
@@ -122,7 +128,7 @@ __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, ui
           const float q0 = __fmul_rn(__fsub_rn(x.x, pa.y), pa.z);
           const float q1 = __fmul_rn(__fsub_rn(x.y, pb.y), pb.z);
           const float r0 = rintf(q0), r1 = rintf(q1);
-          tie |= (fabsf(q0 - r0) > 0.4999f) | (fabsf(q1 - r1) > 0.4999f);
+          tie |= (fabsf(q0 - r0) > TIE) | (fabsf(q1 - r1) > TIE);
           a0 += __float2uint_rn(r0) << (p * BITS);
           a1 += __float2uint_rn(r1) << (p * BITS);
         }
@@ -288,10 +294,17 @@ __global__ void __launch_bounds__(QF_THREADS) qpack_fast_kernel(DevCache c, cons
     tma_bulk_s2g(rec + 2 * G.wbytes + (tsr ? G.kp_bytes : 0) + hf * QF_D * 4, pout, QF_D * 4);
     asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
   }
-  if (tsr == 0)
-    qf_pack<BITS, false>(tile, fs, rec, G, hf);
-  else
-    qf_pack<BITS, true>(tile, fs, rec + G.wbytes, G, hf);
+  if (tsr == 0) {
+    if (G.interleave)
+      qf_pack<BITS, false, true>(tile, fs, rec, G, hf);
+    else
+      qf_pack<BITS, false, false>(tile, fs, rec, G, hf);
+  } else {
+    if (G.interleave)
+      qf_pack<BITS, true, true>(tile, fs, rec + G.wbytes, G, hf);
+    else
+      qf_pack<BITS, true, false>(tile, fs, rec + G.wbytes, G, hf);
+  }
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 
