@@ -206,19 +206,36 @@ def run_ours(args, w, world, rank, local):
     steppers = [bk.DecodeStepper(c, cfg, q, kn, vn, out) for c in reps]
     comm = sharding.SeqSplitComm(world, w["batch"] * w["hq"], D, dev) if seq_split else None
 
+    def qbytes(r):
+        return sum(r.memory().__dict__[f] for f in
+                   ("k_packed_payload_bytes", "v_packed_payload_bytes", "params_bytes"))
+
+    # quantized bytes each step reads, tracked on the host without a C-ABI
+    # call per step: a replica's packed segment grows by one block per cell
+    # when its residual window fills (every cell steps in lockstep)
+    cells = w["batch"] * w["hkv"]
+    blk0 = [r.packed_len(0, 0) // n_r for r in reps]
+    res0 = [r.res_len(0, 0) for r in reps]
+    per_blk = [qbytes(r) // max(1, cells * b) for r, b in zip(reps, blk0)]
+    steps_done = [0] * n_rep
+    for s_ in steppers:
+        s_.prebind(qs, kns, vns)
+
     def one_step(i):
         # inputs of every step are preloaded in HBM (qs/kns/vns slices): the
         # timed region launches only the decode path's own kernels
-        r = reps[i % n_rep]
+        j = i % n_rep
+        r = reps[j]
         if seq_split:
             last = rank == world - 1
             bk.decode_partial(r, cfg, qs[i], kns[i] if last else None,
                               vns[i] if last else None, 0, 1 << 30, out=comm.o, lse=comm.lse)
             comm.merge(out)
-        else:
-            steppers[i % n_rep].step(qs[i], kns[i], vns[i])
-        return sum(r.memory().__dict__[f] for f in
-                   ("k_packed_payload_bytes", "v_packed_payload_bytes", "params_bytes"))
+            return qbytes(r)
+        nbytes = cells * (blk0[j] + (res0[j] + steps_done[j]) // n_r) * per_blk[j]
+        steppers[j].step_pre(i)
+        steps_done[j] += 1
+        return nbytes
 
     # soak (untimed, no append): keeps clocks up while nvidia-smi samples
     clocks = Clocks(local)
@@ -248,6 +265,9 @@ def run_ours(args, w, world, rank, local):
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     n_launched = sum(r.launch_count() for r in reps) - n_launch0 + (K if seq_split else 0)
+    if not seq_split:  # the host-side byte tracking agrees with the cache
+        for j, r in enumerate(reps):
+            assert qbytes(r) == cells * (blk0[j] + (res0[j] + steps_done[j]) // n_r) * per_blk[j]
     # isolated kernel timing: CUDA events bracket every attention launch (this
     # serializes the launches, so it runs after the timed region)
     for r in reps:

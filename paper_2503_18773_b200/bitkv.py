@@ -531,6 +531,20 @@ class DecodeStepper:
         if st:
             _check(st)
 
+    def prebind(self, qs, ks, vs, stream=None) -> None:
+        """Pointer arguments for a preloaded input sequence (qs[i], ks[i],
+        vs[i] stay alive in the caller), for :meth:`step_pre`."""
+        self._pre = [(C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()), C.c_void_p(v.data_ptr()))
+                     for q, k, v in zip(qs, ks, vs)]
+        self._pre_stream = stream if stream is not None else _stream_ptr()
+
+    def step_pre(self, i: int) -> None:
+        """The decode step on the i-th prebound inputs: one C-ABI call."""
+        a, p = self._args, self._pre[i]
+        st = self._fn(a[0], a[1], p[0], p[1], p[2], a[5], self._pre_stream)
+        if st:
+            _check(st)
+
     def step(self, q, k_new, v_new, stream=None) -> None:
         """Same call on other (contiguous CUDA fp16, same-shape) input
         tensors, e.g. one preloaded slice per step; writes the bound out."""
