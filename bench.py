@@ -155,6 +155,14 @@ def run_ours(args, w, world, rank, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     seq_split = args.workload == "C5" and world > 1
+    # C3 at N > 1: KV-head sharding (BASELINE configs[2]); rank p owns KV
+    # heads [p*hkv/N, (p+1)*hkv/N) and their query heads, no data-path
+    # communication (sharding.head_range)
+    head_shard = args.workload == "C3" and world > 1
+    if head_shard:
+        h_lo, h_hi = sharding.head_range(w["hkv"], world, rank)
+        ng = w["hq"] // w["hkv"]
+        w = dict(w, hkv=h_hi - h_lo, hq=(h_hi - h_lo) * ng)
     props = torch.cuda.get_device_properties(dev)
     l2 = getattr(props, "L2_cache_size", 126 * 2**20)
     spec = bk.QuantSpec(w["bits"], bk.QuantAxis.KChannel, w["g"])
@@ -338,13 +346,14 @@ def run_ours(args, w, world, rank, local):
         "metric": METRIC, "value": round(gbs, 1), "unit": "GB/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": round(ms / K, 5),
         "latency_us": round(ms / K * 1e3, 2), "higher_is_better": True,
-        "scaling": "strong" if seq_split else "weak", "vs_baseline": None,
+        "scaling": "strong" if (seq_split or head_shard) else "weak", "vs_baseline": None,
         "dtype": f"u{w['bits']} codes -> fp16 MMA, fp32 accumulate", "data": "synthetic",
         "config": {"workload": f"{args.workload}: {w['desc']}", "batch_per_gpu": w["batch"],
-                   "global_batch": w["batch"] * (1 if seq_split else world),
+                   "global_batch": w["batch"] * (1 if (seq_split or head_shard) else world),
                    "seq_len": w["seq"], "bits": w["bits"], "group_size": w["g"],
                    "warp_n": w["warp_n"], "n_r": n_r,
                    "parallelism": (f"seq-split{world} (NCCL all-gather of (o,lse))" if seq_split
+                                   else f"kv-head-shard{world} (no communication)" if head_shard
                                    else (f"dp{world} (independent batches)" if world > 1
                                          else "single GPU")),
                    "l2": f"rotating {n_rep} cache replicas x {per_rep/1e6:.1f} MB quantized "
