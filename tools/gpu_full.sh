@@ -8,7 +8,7 @@ nvidia-smi -L > $O/gpu.txt 2>&1; lscpu > $O/host_cpu.txt 2>&1
 timeout 1200 python -m pytest tests -m gpu -q -rA > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 900 python bench.py > $O/bench_C2.json 2> $O/bench_C2.err
-for w in C5 C3 C1; do timeout 600 python bench.py --workload $w --no-cpu-baseline > $O/bench_$w.json 2> $O/bench_$w.err; done
+for w in C5 C3 C1 C2b4; do timeout 600 python bench.py --workload $w --no-cpu-baseline > $O/bench_$w.json 2> $O/bench_$w.err; done
 for w in C4 C4b2; do timeout 600 python bench.py --workload $w --steps 100 > $O/bench_$w.json 2> $O/bench_$w.err; done
 timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > $O/bench_ref_C2.json 2> $O/bench_ref_C2.err
 timeout 900 python bench.py --impl reference --workload C5 --steps 3 --warmup 1 > $O/bench_ref_C5.json 2> $O/bench_ref_C5.err
