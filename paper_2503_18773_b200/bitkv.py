@@ -133,8 +133,13 @@ class AttentionConfig:
         return self.heads_q // self.heads_kv
 
     def _c(self) -> _L.AttnConfig:
-        return _L.AttnConfig(self.batch, self.heads_q, self.heads_kv, self.head_dim, self.tile_m,
-                             self.tile_n, self.num_splits, self.warp_n, self.warp_m)
+        key = (self.batch, self.heads_q, self.heads_kv, self.head_dim, self.tile_m, self.tile_n,
+               self.num_splits, self.warp_n, self.warp_m)
+        cached = self.__dict__.get("_c_cache")
+        if cached is None or cached[0] != key:  # the fields are plain and mutable
+            cached = (key, _L.AttnConfig(*key))
+            self.__dict__["_c_cache"] = cached
+        return cached[1]
 
 
 def validate_config(cfg: AttentionConfig) -> AttentionConfig:
@@ -472,6 +477,15 @@ def load_cache_file(path: str, *, max_tokens: int = 0, device: int = 0) -> KVCac
     return KVCache._adopt(h, header, device)
 
 
+def _addr(a: np.ndarray) -> int:
+    """Data address of a C-contiguous array (the cheap way for writable
+    buffers; ``ndarray.ctypes`` builds an object per access)."""
+    try:
+        return C.addressof(C.c_byte.from_buffer(a))
+    except (TypeError, ValueError):
+        return a.ctypes.data
+
+
 def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None) -> AttnOutput:
     """decode_step (attention.hpp:87-88, attention.cpp:164-242).
 
@@ -490,8 +504,8 @@ def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None)
             raise ShapeError("decode_step: q must be [batch, heads_q, d], k_new/v_new "
                              "[batch, heads_kv, d]")
         o = np.empty(shape_q, np.float32)
-        _check(_L.load().bdk_decode_step_host(cache.handle(), C.byref(c), qh.ctypes.data,
-                                              kh.ctypes.data, vh.ctypes.data, o.ctypes.data))
+        _check(_L.load().bdk_decode_step_host(cache.handle(), C.byref(c), _addr(qh), _addr(kh),
+                                              _addr(vh), _addr(o)))
         return AttnOutput(cfg.batch, cfg.heads_q, cfg.head_dim, o)
     if tuple(q.shape) != shape_q or tuple(k_new.shape) != shape_kv or \
             tuple(v_new.shape) != shape_kv:
