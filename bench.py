@@ -212,7 +212,11 @@ def run_ours(args, w, world, rank, local):
     out = torch.empty((w["batch"], w["hq"], D), device=dev, dtype=torch.float32)
     lse = torch.empty((w["batch"], w["hq"]), device=dev, dtype=torch.float32)
     steppers = [bk.DecodeStepper(c, cfg, q, kn, vn, out) for c in reps]
-    comm = sharding.SeqSplitComm(world, w["batch"] * w["hq"], D, dev) if seq_split else None
+    rows = w["batch"] * w["hq"]
+    comm = None
+    if seq_split:  # the exchange: peer-memory merge kernel (default) or NCCL all-gather
+        comm = (sharding.PeerSeqSplit(world, rank, rows, D, dev) if args.exchange == "p2p"
+                else sharding.SeqSplitComm(world, rows, D, dev))
 
     def qbytes(r):
         return sum(r.memory().__dict__[f] for f in
@@ -236,8 +240,13 @@ def run_ours(args, w, world, rank, local):
         r = reps[j]
         if seq_split:
             last = rank == world - 1
+            if args.exchange == "p2p":
+                o_s, lse_s = comm.next_slot()
+                o_s, lse_s = o_s.view(w["batch"], w["hq"], D), lse_s.view(w["batch"], w["hq"])
+            else:
+                o_s, lse_s = comm.o, comm.lse
             bk.decode_partial(r, cfg, qs[i], kns[i] if last else None,
-                              vns[i] if last else None, 0, 1 << 30, out=comm.o, lse=comm.lse)
+                              vns[i] if last else None, 0, 1 << 30, out=o_s, lse=lse_s)
             comm.merge(out)
             return qbytes(r)
         nbytes = cells * (blk0[j] + (res0[j] + steps_done[j]) // n_r) * per_blk[j]
@@ -352,7 +361,9 @@ def run_ours(args, w, world, rank, local):
                    "global_batch": w["batch"] * (1 if (seq_split or head_shard) else world),
                    "seq_len": w["seq"], "bits": w["bits"], "group_size": w["g"],
                    "warp_n": w["warp_n"], "n_r": n_r,
-                   "parallelism": (f"seq-split{world} (NCCL all-gather of (o,lse))" if seq_split
+                   "parallelism": ((f"seq-split{world} (peer-memory merge kernel over NVLink)"
+                                    if args.exchange == "p2p" else
+                                    f"seq-split{world} (NCCL all-gather of (o,lse))") if seq_split
                                    else f"kv-head-shard{world} (no communication)" if head_shard
                                    else (f"dp{world} (independent batches)" if world > 1
                                          else "single GPU")),
@@ -649,6 +660,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--soak", type=float, default=1.0, help="untimed seconds before timing")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="C5 sequence split: peer-memory merge kernel or NCCL all-gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=3)
     args = ap.parse_args()

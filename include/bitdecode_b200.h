@@ -174,6 +174,19 @@ BDK_API bdk_status bdk_decode_partial(bdk_cache* cache, const bdk_attn_config* c
 BDK_API bdk_status bdk_merge_partials(const float* o_dev, const float* lse_dev, uint32_t n_parts,
                                       uint32_t rows, uint32_t d, uint64_t o_stride,
                                       uint64_t lse_stride, float* out_dev, void* stream);
+/* Sequence-split exchange over peer memory, one launch per rank (the
+ * all-gather + combine of attention.cpp:142-162 without NCCL): parts[p]
+ * points at rank p's partial for this step ([rows*d] o then [rows] lse, as
+ * bdk_decode_partial wrote it; a peer-mapped pointer for p != rank) and
+ * flags[p] at rank p's u32 step counter.  The kernel publishes `step` in
+ * flags[rank], waits until every peer's flag reaches it, reads the peers'
+ * partials directly and LSE-merges into out [rows][d] (and out_lse).  Each
+ * rank keeps two slots and uses slot step % 2.  A peer that does not publish
+ * within timeout_ns (0 = 2 s) sets *err = 1 instead of hanging. */
+BDK_API bdk_status bdk_peer_merge(const float* const* parts, uint32_t* const* flags,
+                                  uint32_t world, uint32_t rank, uint64_t step, uint32_t rows,
+                                  uint32_t d, float* out_dev, float* out_lse_dev, int* err_dev,
+                                  uint64_t timeout_ns, void* stream);
 /* 0 = fast (fp16 P), 1 = precise PV (P = P_hi + P_lo) */
 BDK_API bdk_status bdk_set_precise(bdk_cache* cache, int precise);
 

@@ -47,6 +47,8 @@ SIGNATURES = {
     "bdk_prefill": (C.c_int, [vp, u32, u32, vp, vp, u32, vp]),
     "bdk_prefill_all": (C.c_int, [vp, vp, vp, u32, vp]),
     "bdk_cache_reset": (C.c_int, [vp, vp]),
+    "bdk_peer_merge": (C.c_int, [C.POINTER(vp), C.POINTER(vp), u32, u32, C.c_uint64, u32, u32, vp,
+                                 vp, vp, C.c_uint64, vp]),
     "bdk_dump_cache": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(C.c_uint64)]),
     "bdk_load_cache": (C.c_int, [vp, C.c_uint64, u32, C.c_int32, C.POINTER(vp)]),
     "bdk_dump_cache_file": (C.c_int, [vp, C.c_char_p]),

@@ -649,6 +649,32 @@ bdk_status bdk_merge_partials(const float* o, const float* lse, uint32_t n_parts
   return BDK_OK;
 }
 
+bdk_status bdk_peer_merge(const float* const* parts, uint32_t* const* flags, uint32_t world,
+                          uint32_t rank, uint64_t step, uint32_t rows, uint32_t d, float* out,
+                          float* out_lse, int* err, uint64_t timeout_ns, void* stream) {
+  if (world == 0 || world > (uint32_t)bdk::kMaxPeers)
+    return fail(BDK_CONFIG_ERROR, "peer_merge: world must be 1..8");
+  if (rank >= world) return fail(BDK_CONFIG_ERROR, "peer_merge: rank out of range");
+  if (!parts || !flags || !out || !err) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  bdk::PeerMergeArgs a;
+  for (uint32_t p = 0; p < world; ++p) {
+    if (!parts[p] || !flags[p]) return fail(BDK_INVALID_ARGUMENT, "null peer pointer");
+    a.parts[p] = parts[p];
+    a.flags[p] = flags[p];
+  }
+  a.world = (int)world;
+  a.rank = (int)rank;
+  a.step = (long long)step;
+  a.rows = (int)rows;
+  a.d = (int)d;
+  a.out = out;
+  a.out_lse = out_lse;
+  a.err = err;
+  a.timeout_ns = timeout_ns ? timeout_ns : 2000000000ull;
+  BDK_CUDA(bdk::launch_peer_merge(a, as_stream(stream)), "peer merge launch");
+  return BDK_OK;
+}
+
 bdk_status bdk_set_precise(bdk_cache* c, int precise) {
   if (!c) return fail(BDK_INVALID_ARGUMENT, "null cache");
   c->precise = precise ? 1 : 0;

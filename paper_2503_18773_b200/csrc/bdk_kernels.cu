@@ -647,6 +647,66 @@ __global__ void merge_partials_kernel(const float* o, const float* lse, int n_pa
   }
 }
 
+// Sequence-split exchange over peer memory.
+// Rank r's normalized partial [rows*d o | rows lse] (bdk_decode_partial)
+// sits in slot step%2 of its own buffer; one launch per rank (1) publishes
+// "rank r has step s" with a system-scope release of its monotonic step flag
+// (the partial was written by the previous kernel in this stream), (2) waits
+// for every peer's flag with system-scope acquires, (3) reads the peers'
+// partials straight from their HBM (NVLink P2P loads through the peer
+// mapping; plain loads for the local rank) and LSE-merges them (combine,
+// attention.cpp:142-162).  Two slots suffice: a rank can only reach step s+2
+// after its step s+1 merge saw every peer publish s+1, which each peer does
+// after finishing its own step-s merge.  A stuck peer trips the timeout and
+// sets *err instead of hanging the GPU.
+__global__ void __launch_bounds__(128) peer_merge_kernel(PeerMergeArgs a) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) {
+      __threadfence_system();
+      asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(a.flags[a.rank]),
+                   "r"((unsigned)a.step)
+                   : "memory");
+    }
+    int good = 1;
+    const unsigned long long t0 = globaltimer();
+    for (int p = 0; p < a.world && good; ++p) {
+      if (p == a.rank) continue;
+      for (;;) {
+        unsigned v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(a.flags[p]) : "memory");
+        if ((int)(v - (unsigned)a.step) >= 0) break;  // monotonic step counter, wrap-safe
+        if (globaltimer() - t0 > a.timeout_ns) {
+          good = 0;
+          atomicExch(a.err, 1);
+          break;
+        }
+        __nanosleep(100);
+      }
+    }
+    ok = good;
+  }
+  __syncthreads();
+  if (!ok) return;
+  const int rows = a.rows, d = a.d;
+  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+    float ms = -INFINITY;
+    for (int p = 0; p < a.world; ++p) ms = fmaxf(ms, __ldcv(a.parts[p] + (size_t)rows * d + row));
+    for (int ch = threadIdx.x; ch < d; ch += blockDim.x) {
+      float acc = 0.f, l = 0.f;
+      for (int p = 0; p < a.world; ++p) {
+        const float m = __ldcv(a.parts[p] + (size_t)rows * d + row);
+        if (m == -INFINITY) continue;
+        const float w = ex2(m - ms);
+        acc = fmaf(__ldcv(a.parts[p] + (size_t)row * d + ch), w, acc);
+        l += w;
+      }
+      a.out[(size_t)row * d + ch] = l > 0.f ? acc / l : 0.f;
+      if (a.out_lse != nullptr && ch == 0) a.out_lse[row] = l > 0.f ? ms + __log2f(l) : -INFINITY;
+    }
+  }
+}
+
 // ------------------------------------------------------------- launchers
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device,
@@ -823,6 +883,12 @@ cudaError_t launch_dequant(const DevCache& c, int cell, int blk0, int nblk, __ha
 cudaError_t launch_merge_partials(const float* o, const float* lse, int n_parts, int rows, int d,
                                   size_t o_stride, size_t lse_stride, float* out, cudaStream_t s) {
   merge_partials_kernel<<<rows, 128, 0, s>>>(o, lse, n_parts, rows, d, o_stride, lse_stride, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_merge(const PeerMergeArgs& a, cudaStream_t s) {
+  const int grid = std::max(1, std::min(a.rows, 16));  // few CTAs: never crowd out a peer
+  peer_merge_kernel<<<grid, 128, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -94,6 +94,21 @@ cudaError_t launch_dequant(const DevCache& c, int cell, int blk0, int nblk, __ha
                            __half* v_out, cudaStream_t s);
 // merge normalized (o, lse) partials of n_parts ranks: o [n_parts][rows][d],
 // lse [n_parts][rows] (log2 domain) -> out [rows][d]
+// sequence-split exchange over peer memory (bdk_peer_merge)
+constexpr int kMaxPeers = 8;
+struct PeerMergeArgs {
+  const float* parts[kMaxPeers];  // slot of each rank: [rows*d o | rows lse] (peer-mapped)
+  unsigned* flags[kMaxPeers];     // each rank's monotonic step flag (peer-mapped)
+  int world = 1, rank = 0;
+  long long step = 0;
+  int rows = 0, d = 0;
+  float* out = nullptr;
+  float* out_lse = nullptr;
+  int* err = nullptr;
+  unsigned long long timeout_ns = 0;
+};
+cudaError_t launch_peer_merge(const PeerMergeArgs& a, cudaStream_t s);
+
 cudaError_t launch_merge_partials(const float* o, const float* lse, int n_parts, int rows, int d,
                                   size_t o_stride, size_t lse_stride, float* out, cudaStream_t s);
 

@@ -14,6 +14,9 @@ One process per GPU, ``torch.distributed`` over NCCL for the plumbing.
   exchanges them and every rank LSE-merges locally (``bdk_merge_partials``,
   the math of combine, attention.cpp:142-162).  Results are split-invariant
   within the reference's own tolerance (test_attention.cpp:312-340).
+  ``PeerSeqSplit`` does the same exchange without NCCL: every rank's merge
+  kernel reads the peers' partials straight out of their HBM over NVLink
+  (bdk_peer_merge); ``SeqSplitComm`` is the NCCL all-gather version.
 """
 from __future__ import annotations
 
@@ -80,3 +83,90 @@ class SeqSplitComm:
         from . import bitkv
         o_parts, lse_parts = self.exchange()
         return bitkv.merge_partials(o_parts, lse_parts, out=out.view(self.rows, self.d))
+
+
+class PeerSeqSplit:
+    """Sequence-split exchange over peer memory: one ``bdk_peer_merge`` launch
+    per rank and step, no collective library on the data path.
+
+    Every rank owns a buffer of two slots ``[2, rows*d + rows]`` (fp32 o then
+    lse, the layout ``bdk_decode_partial`` writes) and a u32 step flag.  Step s
+    (1, 2, ...) uses slot s % 2: ``next_slot()`` returns the (o, lse) views the
+    rank's partial decode writes, then ``merge(out)`` publishes the step and
+    merges every rank's slot into ``out``.  Across processes the buffers and
+    flags are shared with CUDA IPC (torch's tensor reductions, exchanged once
+    with ``all_gather_object``); peers on other GPUs are reached through the
+    peer mapping the IPC open enables.  ``local_group`` builds the ranks of
+    one process (e.g. one GPU, one stream per rank) for tests."""
+
+    def __init__(self, world: int, rank: int, rows: int, d: int, device, group=None,
+                 _shared=None, timeout_s: float = 2.0):
+        import torch
+        self.world, self.rank, self.rows, self.d = world, rank, rows, d
+        self.part = rows * d + rows
+        self.buf = torch.zeros((2, self.part), dtype=torch.float32, device=device)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        self.timeout_ns = int(timeout_s * 1e9)
+        self.step = 0
+        self._keep = []
+        if _shared is None:
+            _shared = [(self.buf, self.flag)] if world == 1 else self._exchange(group)
+        self._bind(_shared)
+
+    def _exchange(self, group):
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        mine = (reduce_tensor(self.buf), reduce_tensor(self.flag))
+        objs = [None] * self.world
+        dist.all_gather_object(objs, mine, group=group)
+        shared = []
+        for p, (rb, rf) in enumerate(objs):
+            if p == self.rank:
+                shared.append((self.buf, self.flag))
+            else:
+                shared.append((rb[0](*rb[1]), rf[0](*rf[1])))
+        return shared
+
+    def _bind(self, shared):
+        import ctypes as C
+        self._keep = shared
+        W = C.c_void_p * self.world
+        self._parts = [W(*[b[slot].data_ptr() for b, _ in shared]) for slot in (0, 1)]
+        self._flags = W(*[f.data_ptr() for _, f in shared])
+
+    @classmethod
+    def local_group(cls, world: int, rows: int, d: int, device) -> list["PeerSeqSplit"]:
+        """All ranks of one process sharing plain device pointers."""
+        ranks = [cls(1, 0, rows, d, device) for _ in range(world)]
+        shared = [(r.buf, r.flag) for r in ranks]
+        for i, r in enumerate(ranks):
+            r.world, r.rank = world, i
+            r._bind(shared)
+        return ranks
+
+    def next_slot(self):
+        """(o [rows, d], lse [rows]) views this rank's partial of the next step
+        is written into."""
+        slot = self.buf[(self.step + 1) % 2]
+        return slot[: self.rows * self.d].view(self.rows, self.d), slot[self.rows * self.d:]
+
+    def merge(self, out, out_lse=None, stream=None) -> None:
+        """Publish the next step and LSE-merge every rank's partial into out."""
+        import ctypes as C
+        from . import _lib as L
+        from . import bitkv
+        self.step += 1
+        vp = C.c_void_p
+        st = L.load().bdk_peer_merge(
+            self._parts[self.step % 2], self._flags, self.world, self.rank, self.step, self.rows,
+            self.d, vp(out.data_ptr()), vp(out_lse.data_ptr()) if out_lse is not None else None,
+            vp(self.err.data_ptr()), self.timeout_ns,
+            stream if stream is not None else bitkv._stream_ptr())
+        bitkv._check(st)
+
+    def check(self) -> None:
+        """Raise if a merge timed out waiting for a peer (reads the device flag)."""
+        from . import bitkv
+        if int(self.err.item()):
+            raise bitkv.CudaError("peer_merge: a peer did not publish its partial in time")

@@ -361,3 +361,45 @@ def test_partial_ranges_merge_to_full_decode(parts, precise):
         assert err < 1e-5, err
     else:
         check_tol(errors(merged.cpu().numpy(), full_o.cpu().numpy()), False)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_merge_sequence_split_on_streams(world):
+    """Sequence split with the peer-memory exchange (bdk_peer_merge): the
+    ranks run in one process on one GPU, one stream each, so the merge kernels
+    genuinely wait on each other's step flags.  Every rank's merged output
+    equals the full decode (precise mode: the reference's 1e-5), over several
+    steps so both slots and the monotonic flags are exercised."""
+    bk = _bk()
+    from oracle import oracle as O
+    from paper_2503_18773_b200 import sharding
+    c = Case(bits=4, warp_n=4, heads_q=32, heads_kv=8, batch=1, prefill=24 * 128 + 45, seed=9)
+    g = O.Gauss(c.seed)
+    k, v = prefill_data(c, g)
+    gc = gpu_cache(c, k, v)
+    gc.set_precise(True)
+    cfg = bk.AttentionConfig(batch=1, heads_q=32, heads_kv=8, head_dim=D, warp_n=4)
+    rows = 32
+    comms = sharding.PeerSeqSplit.local_group(world, rows, D, torch.device("cuda"))
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    outs = [torch.empty((rows, D), dtype=torch.float32, device="cuda") for _ in range(world)]
+    lses = [torch.empty(rows, dtype=torch.float32, device="cuda") for _ in range(world)]
+    nblk = gc.packed_len(0, 0) // gc.n_r()
+    for _ in range(3):
+        q, _, _ = step_data(c, g)
+        qd = torch.from_numpy(q).cuda().half()
+        full_o, full_lse = bk.decode_partial(gc, cfg, qd)
+        torch.cuda.synchronize()
+        for r in range(world):  # launch order: every rank's merge waits on its peers
+            lo, hi = sharding.block_range(nblk, world, r)
+            with torch.cuda.stream(streams[r]):
+                o, lse = comms[r].next_slot()
+                bk.decode_partial(gc, cfg, qd, None, None, lo, hi, out=o.view(1, rows, D),
+                                  lse=lse.view(1, rows), include_residual=(r == world - 1))
+                comms[r].merge(outs[r], lses[r])
+        torch.cuda.synchronize()
+        for r in range(world):
+            comms[r].check()
+            err = (outs[r] - full_o.view(rows, D)).abs().max().item()
+            assert err < 1e-5, (r, err)
+            assert (lses[r] - full_lse.view(rows)).abs().max().item() < 1e-4

@@ -103,3 +103,64 @@ def test_seq_split_exchange_and_merge_over_gloo(world):
     full, _ = _partial(q, k, v)
     for r in range(world):
         np.testing.assert_allclose(results[r], full, atol=1e-5, rtol=0)
+
+
+def _peer_worker(rank, world, port, data, out_q):
+    """One process per rank on ONE GPU: the peer-memory exchange with its
+    buffers and flags shared over CUDA IPC (the multi-GPU plumbing of
+    PeerSeqSplit).  Partials are computed on the host (numpy) and copied into
+    this rank's slot; bdk_peer_merge does the exchange + merge."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        q, k, v, n_r = data
+        nblk = k.shape[0] // n_r
+        lo, hi = sharding.block_range(nblk, world, rank)
+        t_hi = hi * n_r if rank < world - 1 else k.shape[0]
+        comm = sharding.PeerSeqSplit(world, rank, q.shape[0], q.shape[1], torch.device("cuda", 0),
+                                     timeout_s=20.0)
+        outs = []
+        for step in range(2):
+            o, lse = _partial(q * (step + 1), k[lo * n_r:t_hi], v[lo * n_r:t_hi])
+            so, sl = comm.next_slot()
+            so.copy_(torch.from_numpy(o.astype(np.float32)))
+            sl.copy_(torch.from_numpy(lse.astype(np.float32)))
+            out = torch.empty((q.shape[0], q.shape[1]), dtype=torch.float32, device="cuda")
+            comm.merge(out)
+            torch.cuda.synchronize()
+            comm.check()
+            outs.append(out.cpu().numpy().astype(np.float64))
+        dist.barrier()  # peers keep their buffers mapped until everyone is done
+        out_q.put((rank, outs))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_peer_merge_across_processes_over_cuda_ipc():
+    import torch.multiprocessing as mp
+    world = 2
+    rng = np.random.default_rng(1)
+    n_r, d, rows = 128, 128, 4
+    length = 6 * n_r + 11
+    q = rng.standard_normal((rows, d))
+    k = rng.standard_normal((length, d))
+    v = rng.standard_normal((length, d))
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, (q, k, v, n_r), out_q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(out_q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for step in range(2):
+        full, _ = _partial(q * (step + 1), k, v)
+        for r in range(world):
+            np.testing.assert_allclose(results[r][step], full, atol=1e-5, rtol=0)
