@@ -86,7 +86,7 @@ __host__ __device__ inline Smem smem_layout(const Geom& G, int ng, int NS, int g
   L.prep = L.ring + NS * G.rec_bytes;
   L.merge = L.prep + NS * L.prep_stride;
   const uint32_t merge_bytes = (uint32_t)(
-      max(G.warp_n * grp * (col_pack(G, ng) * ng * D + 16), 24 + 2 * MERGE_KC * 8 + 4 * 32 * G.warp_n * grp) *
+      max(G.warp_n * grp * (((ng <= 4 && (G.bits == 2 || G.bits == 4)) ? 2 : 1) * ng * D + 16), 24 + 2 * MERGE_KC * 8 + 4 * 32 * G.warp_n * grp) *
           4 +
       64);
   L.merge_floats = merge_bytes / 4;
@@ -1168,8 +1168,11 @@ static int variant_knob() {
 // groups at 128 registers (both measured 6-15% slower).
 static Variant fast_kernel(const Geom& G, int ng) {
   const int v = variant_knob();
-  static const bool cp_off = getenv("BDK_COLPACK") && atoi(getenv("BDK_COLPACK")) == 0;
-  const int cp = cp_off ? 1 : col_pack(G, ng);
+  // dev knob BDK_COLPACK: 0 = never, 2 = wherever the layout allows (4-bit too)
+  static const int cp_knob = getenv("BDK_COLPACK") ? atoi(getenv("BDK_COLPACK")) : -1;
+  const int cp = cp_knob == 0 ? 1
+                 : cp_knob == 2 ? ((ng <= 4 && (G.bits == 2 || G.bits == 4)) ? 2 : 1)
+                                : col_pack(G, ng);
 #define BDK_SEL(B, W, NS, MB, GR) \
   if (G.bits == B && G.warp_n == W) return variant<B, W, NS, MB, GR>(cp);
   if (v == 2) {
