@@ -197,6 +197,16 @@ BDK_API bdk_status bdk_set_precise(bdk_cache* cache, int precise);
 BDK_API bdk_status bdk_read_block(const bdk_cache* cache, uint32_t b, uint32_t h, uint32_t blk,
                                   uint16_t* k_words, uint16_t* v_words, uint16_t* k_params,
                                   uint16_t* v_params);
+/* KVCache::build_block (kvcache.cpp:208-219): quantize + pack the full
+ * residual into host word/param arrays without committing; StateError unless
+ * res_len == N_r. */
+BDK_API bdk_status bdk_build_block(bdk_cache* cache, uint32_t b, uint32_t h, uint16_t* k_words,
+                                   uint16_t* v_words, uint16_t* k_params, uint16_t* v_params);
+/* KVCache::commit_block (kvcache.cpp:231-237): adopt the block and clear the
+ * residual; StateError unless res_len == N_r. */
+BDK_API bdk_status bdk_commit_block(bdk_cache* cache, uint32_t b, uint32_t h,
+                                    const uint16_t* k_words, const uint16_t* v_words,
+                                    const uint16_t* k_params, const uint16_t* v_params);
 /* KVCache::adopt_block (kvcache.cpp:239-243): append an already-packed block
  * (reference layout, host inputs). */
 BDK_API bdk_status bdk_adopt_block(bdk_cache* cache, uint32_t b, uint32_t h,

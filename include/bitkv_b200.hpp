@@ -341,7 +341,31 @@ class KVCache {  // kvcache.hpp:103-189, cache resident in HBM
     for (size_t i = 0; i < nb; ++i) out.blocks.push_back(block(b, h, i));
     return out;
   }
+  // KVCache::build_block (kvcache.cpp:208-219): pack the full residual on the
+  // device without committing
+  PackedBlock build_block(size_t b, size_t h) {
+    PackedBlock blk = empty_block();
+    detail::check(bdk_build_block(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h),
+                                  blk.k_words.data(), blk.v_words.data(),
+                                  blk.k_params.data.data(), blk.v_params.data.data()));
+    return blk;
+  }
+  // KVCache::commit_block (kvcache.cpp:231-237)
+  void commit_block(size_t b, size_t h, const PackedBlock& blk) {
+    detail::check(bdk_commit_block(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h),
+                                   blk.k_words.data(), blk.v_words.data(),
+                                   blk.k_params.data.data(), blk.v_params.data.data()));
+  }
+
   PackedBlock block(size_t b, size_t h, size_t i) const {
+    PackedBlock blk = empty_block();
+    detail::check(bdk_read_block(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h),
+                                 static_cast<uint32_t>(i), blk.k_words.data(), blk.v_words.data(),
+                                 blk.k_params.data.data(), blk.v_params.data.data()));
+    return blk;
+  }
+  // a block sized for this geometry, params grids as quant.cpp:59-91
+  PackedBlock empty_block() const {
     PackedBlock blk;
     blk.k_words.resize(info_.words_per_block);
     blk.v_words.resize(info_.words_per_block);
@@ -359,9 +383,6 @@ class KVCache {  // kvcache.hpp:103-189, cache resident in HBM
       blk.v_params.rows = n_r();
       blk.v_params.cols = head_dim_ / g;
     }
-    detail::check(bdk_read_block(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h),
-                                 static_cast<uint32_t>(i), blk.k_words.data(), blk.v_words.data(),
-                                 blk.k_params.data.data(), blk.v_params.data.data()));
     return blk;
   }
   // KVCache::residual_tile (kvcache.cpp:253-261): [res_len, d] fp32 each

@@ -66,6 +66,8 @@ SIGNATURES = {
     "bdk_set_precise": (C.c_int, [vp, C.c_int]),
     "bdk_read_block": (C.c_int, [vp, u32, u32, u32, u16p, u16p, u16p, u16p]),
     "bdk_adopt_block": (C.c_int, [vp, u32, u32, u16p, u16p, u16p, u16p]),
+    "bdk_build_block": (C.c_int, [vp, u32, u32, u16p, u16p, u16p, u16p]),
+    "bdk_commit_block": (C.c_int, [vp, u32, u32, u16p, u16p, u16p, u16p]),
     "bdk_read_residual": (C.c_int, [vp, u32, u32, u16p, u16p]),
     "bdk_dequant_blocks": (C.c_int, [vp, u32, u32, u32, u32, vp, vp, vp]),
     "bdk_memory": (C.c_int, [vp, C.POINTER(C.c_uint64)]),

@@ -335,6 +335,27 @@ class KVCache:
         _check(_L.load().bdk_adopt_block(self._h, b, h, _u16p(kw), _u16p(vw), _u16p(kp),
                                          _u16p(vpp)))
 
+    def build_block(self, b: int, h: int) -> PackedBlock:
+        """KVCache::build_block (kvcache.cpp:208-219): the full residual
+        quantized + packed on the device, not committed."""
+        kw = np.zeros(self.info.words_per_block, np.uint16)
+        vw = np.zeros(self.info.words_per_block, np.uint16)
+        kp = np.zeros(self.info.k_param_u16, np.uint16)
+        vpp = np.zeros(self.info.v_param_u16, np.uint16)
+        _check(_L.load().bdk_build_block(self._h, b, h, _u16p(kw), _u16p(vw), _u16p(kp),
+                                         _u16p(vpp)))
+        return PackedBlock(kw, vw, kp, vpp)
+
+    def commit_block(self, b: int, h: int, block: PackedBlock) -> None:
+        """KVCache::commit_block (kvcache.cpp:231-237): append the block and
+        clear the (full) residual."""
+        kw = np.ascontiguousarray(block.k_words, np.uint16)
+        vw = np.ascontiguousarray(block.v_words, np.uint16)
+        kp = np.ascontiguousarray(block.k_params, np.uint16)
+        vpp = np.ascontiguousarray(block.v_params, np.uint16)
+        _check(_L.load().bdk_commit_block(self._h, b, h, _u16p(kw), _u16p(vw), _u16p(kp),
+                                          _u16p(vpp)))
+
     def _lengths(self, b, h):
         p, r = C.c_uint32(), C.c_uint32()
         _check(_L.load().bdk_cache_lengths(self._h, b, h, C.byref(p), C.byref(r)))

@@ -823,13 +823,10 @@ bdk_status bdk_packed_tile_host(const bdk_cache* c, uint32_t b, uint32_t h, uint
   return BDK_OK;
 }
 
-bdk_status bdk_read_block(const bdk_cache* c, uint32_t b, uint32_t h, uint32_t blk,
-                          uint16_t* kw, uint16_t* vw, uint16_t* kp, uint16_t* vp) {
-  bdk_status s = check_cell(c, b, h);
-  if (s) return s;
-  const int i = cell_of(c, b, h);
-  if (static_cast<int>(blk) >= c->packed_blocks[i])
-    return fail(BDK_SHAPE_ERROR, "block index past the packed segment");
+// D2H of one block record (cell i, slot blk), un-swizzled into the
+// reference's word arrays
+static bdk_status read_record(const bdk_cache* c, int i, uint32_t blk, uint16_t* kw,
+                              uint16_t* vw, uint16_t* kp, uint16_t* vp) {
   const Geom& G = c->dev.G;
   std::vector<uint8_t> rec(G.rec_bytes);
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
@@ -845,6 +842,48 @@ bdk_status bdk_read_block(const bdk_cache* c, uint32_t b, uint32_t h, uint32_t b
   }
   if (kp) std::memcpy(kp, rec.data() + 2 * G.wbytes, G.kp_bytes);
   if (vp) std::memcpy(vp, rec.data() + 2 * G.wbytes + G.kp_bytes, G.vp_bytes);
+  return BDK_OK;
+}
+
+bdk_status bdk_read_block(const bdk_cache* c, uint32_t b, uint32_t h, uint32_t blk,
+                          uint16_t* kw, uint16_t* vw, uint16_t* kp, uint16_t* vp) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  const int i = cell_of(c, b, h);
+  if (static_cast<int>(blk) >= c->packed_blocks[i])
+    return fail(BDK_SHAPE_ERROR, "block index past the packed segment");
+  return read_record(c, i, blk, kw, vw, kp, vp);
+}
+
+bdk_status bdk_build_block(bdk_cache* c, uint32_t b, uint32_t h, uint16_t* kw, uint16_t* vw,
+                           uint16_t* kp, uint16_t* vp) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  const int i = cell_of(c, b, h);
+  if (c->res_len[i] != c->dev.G.n_r)
+    return fail(BDK_STATE_ERROR, "build_block requires a full residual (res_len == N_r)");
+  if (c->packed_blocks[i] >= c->dev.G.max_blocks)
+    return fail(BDK_CAPACITY_ERROR, "cache arena full (raise max_tokens)");
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  c->launches += 1;
+  BDK_CUDA(bdk::launch_build(c->dev, i, nullptr), "build launch");
+  c->blocks_written = true;  // the slot past the packed segment was written
+  return read_record(c, i, (uint32_t)c->packed_blocks[i], kw, vw, kp, vp);
+}
+
+bdk_status bdk_commit_block(bdk_cache* c, uint32_t b, uint32_t h, const uint16_t* kw,
+                            const uint16_t* vw, const uint16_t* kp, const uint16_t* vp) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  const int i = cell_of(c, b, h);
+  if (c->res_len[i] != c->dev.G.n_r)
+    return fail(BDK_STATE_ERROR, "commit_block requires a full residual (res_len == N_r)");
+  s = bdk_adopt_block(c, b, h, kw, vw, kp, vp);
+  if (s) return s;
+  const int zero = 0;
+  BDK_CUDA(cudaMemcpy(c->dev.res_len + i, &zero, sizeof(int), cudaMemcpyHostToDevice),
+           "H2D res_len");
+  c->res_len[i] = 0;
   return BDK_OK;
 }
 

@@ -82,14 +82,17 @@ __global__ void append_kernel(DevCache c, int cell, const __half* k_row, const _
 }
 
 template <int BITS>
-__global__ void __launch_bounds__(256) flush_kernel(DevCache c, int cell) {
+__global__ void __launch_bounds__(256) flush_kernel(DevCache c, int cell, int commit) {
+  // flush_residual (commit = 1) / build_block (commit = 0, kvcache.cpp:
+  // 208-219): pack the full residual into the next block slot; only a flush
+  // updates the lengths
   extern __shared__ __align__(128) uint8_t smem[];
   const Geom& G = c.G;
   const int slot = c.packed_blocks[cell];
   uint8_t* rec = c.records + ((size_t)cell * G.max_blocks + slot) * G.rec_bytes;
   const size_t base = (size_t)cell * G.n_r * G.d;
   qpack_block<BITS>(G, c.res_k + base, c.res_v + base, G.d, rec, smem);
-  if (threadIdx.x == 0) {
+  if (commit && threadIdx.x == 0) {
     c.packed_blocks[cell] = slot + 1;
     c.res_len[cell] = 0;
   }
@@ -833,24 +836,32 @@ cudaError_t launch_append(const DevCache& c, int cell, const __half* k_row, cons
 }
 
 template <int BITS>
-static cudaError_t flush_bits(const DevCache& c, int cell, cudaStream_t s) {
+static cudaError_t flush_bits(const DevCache& c, int cell, int commit, cudaStream_t s) {
   const size_t smem = (size_t)c.G.n_r * c.G.d;
   auto kern = flush_kernel<BITS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(std::max<size_t>(smem, 16)));
   if (e != cudaSuccess) return e;
-  kern<<<1, 256, smem, s>>>(c, cell);
+  kern<<<1, 256, smem, s>>>(c, cell, commit);
   return cudaGetLastError();
 }
 
-cudaError_t launch_flush(const DevCache& c, int cell, cudaStream_t s) {
+static cudaError_t flush_any(const DevCache& c, int cell, int commit, cudaStream_t s) {
   switch (c.G.bits) {
-    case 2: return flush_bits<2>(c, cell, s);
-    case 4: return flush_bits<4>(c, cell, s);
-    case 8: return flush_bits<8>(c, cell, s);
-    case 16: return flush_bits<16>(c, cell, s);
+    case 2: return flush_bits<2>(c, cell, commit, s);
+    case 4: return flush_bits<4>(c, cell, commit, s);
+    case 8: return flush_bits<8>(c, cell, commit, s);
+    case 16: return flush_bits<16>(c, cell, commit, s);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_flush(const DevCache& c, int cell, cudaStream_t s) {
+  return flush_any(c, cell, 1, s);
+}
+
+cudaError_t launch_build(const DevCache& c, int cell, cudaStream_t s) {
+  return flush_any(c, cell, 0, s);
 }
 
 template <int BITS>

@@ -88,6 +88,7 @@ cudaError_t launch_prefill(const DevCache& c, const __half* k, const __half* v, 
 cudaError_t launch_append(const DevCache& c, int cell, const __half* k_row, const __half* v_row,
                           cudaStream_t s);
 cudaError_t launch_flush(const DevCache& c, int cell, cudaStream_t s);
+cudaError_t launch_build(const DevCache& c, int cell, cudaStream_t s);  // pack, no commit
 cudaError_t launch_decode(const DevCache& c, const DecodeArgs& a, cudaStream_t s);
 // dequantize blocks [blk0, blk0+nblk) of a cell into fp16 [nblk*n_r][d] rows
 cudaError_t launch_dequant(const DevCache& c, int cell, int blk0, int nblk, __half* k_out,

@@ -195,6 +195,42 @@ def test_residual_flush_happens_on_the_nth_step():
     assert gc.packed_len(0, 0) == n_r and gc.res_len(0, 0) == 0
 
 
+@pytest.mark.parametrize("bits", [2, 4])
+def test_build_then_commit_block(bits):
+    """build_block / commit_block (kvcache.cpp:208-237, the decode step's
+    cache-update split, attention.cpp:103, :235-240): build packs the full
+    residual bit-exactly without changing the cell; commit appends it and
+    clears the residual; build on a partial residual is a StateError."""
+    bk = _bk()
+    from oracle import oracle as O
+    c = Case(bits=bits, warp_n=4, heads_kv=1, batch=1, prefill=2 * (8 * 4 * (16 // bits)) + 5,
+             seed=60 + bits)
+    g = O.Gauss(c.seed)
+    k, v = prefill_data(c, g)
+    gc, oc = gpu_cache(c, k, v), oracle_cache(c, k, v)
+    n_r = gc.n_r()
+    with pytest.raises(bk.StateError):
+        gc.build_block(0, 0)
+    while gc.res_len(0, 0) < n_r:
+        kr = g.rounded(D)
+        vr = g.rounded(D)
+        gc.append_token(0, 0, torch.from_numpy(kr).cuda().half(), torch.from_numpy(vr).cuda().half())
+        oc.append_token(0, 0, kr, vr)
+    p0 = gc.packed_len(0, 0)
+    blk = gc.build_block(0, 0)
+    assert gc.packed_len(0, 0) == p0 and gc.res_len(0, 0) == n_r  # nothing committed
+    oc.flush_residual(0, 0)
+    kw, vw, kp, vp = oc.block(0, 0, p0 // n_r)
+    assert np.array_equal(blk.k_words, kw) and np.array_equal(blk.v_words, vw)
+    assert np.array_equal(blk.k_params, kp) and np.array_equal(blk.v_params, vp)
+    gc.commit_block(0, 0, blk)
+    assert gc.packed_len(0, 0) == p0 + n_r and gc.res_len(0, 0) == 0
+    got = gc.block(0, 0, p0 // n_r)
+    assert np.array_equal(got.k_words, kw) and np.array_equal(got.v_params, vp)
+    with pytest.raises(bk.StateError):
+        gc.commit_block(0, 0, blk)
+
+
 def test_long_context_c1_shape():
     """BASELINE configs[0] shape (LLaMA-3.1-8B, 4K, 4-bit g128 N_r 128)."""
     c = Case(bits=4, warp_n=4, heads_q=32, heads_kv=8, batch=1, prefill=4096, steps=3, seed=1)
