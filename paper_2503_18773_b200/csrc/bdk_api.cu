@@ -697,7 +697,7 @@ __attribute__((target("avx,f16c"))) void f32_to_f16_f16c(const float* in, uint16
   for (; i < n; ++i) out[i] = static_cast<uint16_t>(_cvtss_sh(in[i], _MM_FROUND_TO_NEAREST_INT));
 }
 
-void f32_to_f16_host(const float* in, uint16_t* out, size_t n) {
+void f32_to_f16_serial(const float* in, uint16_t* out, size_t n) {
   static const bool f16c = __builtin_cpu_supports("f16c") && __builtin_cpu_supports("avx");
   if (f16c) {
     f32_to_f16_f16c(in, out, n);
@@ -706,6 +706,38 @@ void f32_to_f16_host(const float* in, uint16_t* out, size_t n) {
   for (size_t i = 0; i < n; ++i) {
     const __half h = __float2half_rn(in[i]);
     std::memcpy(out + i, &h, 2);
+  }
+}
+
+// large host tensors (e.g. b32 MHA: 1.5 MB of fp32 inputs per step) are
+// converted / copied by several host threads: a single core's memory
+// bandwidth would otherwise dominate the host-API step
+constexpr size_t kParallelHost = size_t(1) << 17;  // elements
+constexpr int kHostThreads = 8;
+
+void f32_to_f16_host(const float* in, uint16_t* out, size_t n) {
+  if (n < kParallelHost) {
+    f32_to_f16_serial(in, out, n);
+    return;
+  }
+  const size_t chunk = (n / kHostThreads + 7) & ~size_t(7);
+#pragma omp parallel for num_threads(kHostThreads) schedule(static)
+  for (int t = 0; t < kHostThreads; ++t) {
+    const size_t lo = std::min(n, (size_t)t * chunk), hi = std::min(n, lo + chunk);
+    if (hi > lo) f32_to_f16_serial(in + lo, out + lo, hi - lo);
+  }
+}
+
+void copy_host(float* dst, const float* src, size_t n) {
+  if (n < kParallelHost) {
+    std::memcpy(dst, src, n * 4);
+    return;
+  }
+  const size_t chunk = (n / kHostThreads + 15) & ~size_t(15);
+#pragma omp parallel for num_threads(kHostThreads) schedule(static)
+  for (int t = 0; t < kHostThreads; ++t) {
+    const size_t lo = std::min(n, (size_t)t * chunk), hi = std::min(n, lo + chunk);
+    if (hi > lo) std::memcpy(dst + lo, src + lo, (hi - lo) * 4);
   }
 }
 }  // namespace
@@ -747,7 +779,7 @@ bdk_status bdk_decode_step_host(bdk_cache* c, const bdk_attn_config* cfg, const 
   if (s) return s;
   if (!zc) BDK_CUDA(cudaMemcpyAsync(hout, dout, nq * 4, cudaMemcpyDeviceToHost, st), "D2H");
   BDK_CUDA(cudaStreamSynchronize(st), "decode_step_host");
-  std::memcpy(out, hout, nq * 4);
+  copy_host(out, hout, nq);
   return BDK_OK;
 }
 
