@@ -1,6 +1,6 @@
 """bench.py -- BitDecoding decode hot path on B200: quantized-KV decode attention.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2|C5|C3|C1|C2b4|C4|C4b2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2|C5|C3|C1|C2w2|C2b4|C4|C4b2]
                     [--impl ours|reference] [--no-cpu-baseline] [--extra]
 
 Prints ONE JSON line (rank 0).  The metric is BASELINE.json's: decode-attention
@@ -51,6 +51,10 @@ WORKLOADS = {
                desc="LLaMA-2-7B MHA decode attn, b32, 32q/32kv, d128, 4-bit g128 N_r128, 8K"),
     "C5": dict(batch=1, hq=32, hkv=8, bits=4, warp_n=4, g=128, seq=131072,
                desc="LLaMA-3.1-8B decode attn, b1, 32q/8kv, d128, 4-bit g128 N_r128, 128K"),
+    # C2 with the 128-token fp16 residual of configs[0] ("same shape"): 2-bit
+    # at W_n = 2 gives N_r = 128 (layout.cpp:74-77)
+    "C2w2": dict(batch=8, hq=32, hkv=8, bits=2, warp_n=2, g=128, seq=32768,
+                 desc="LLaMA-3.1-8B decode attn, b8, 32q/8kv, d128, 2-bit g128 N_r128 (W_n 2), 32K"),
     # the north-star statement's 4-bit case at the C2 shape (not a BASELINE
     # config): LLaMA-3.1-8B, 4-bit, batch 8, 32K
     "C2b4": dict(batch=8, hq=32, hkv=8, bits=4, warp_n=4, g=128, seq=32768,
@@ -631,7 +635,7 @@ def run_reference_arm(args, w, world, rank):
                         "d2h_bytes_per_step": 0}}
     steps = args.steps
     # bound the run: the reference step at C2/C5 is ~1 s on 8 cores
-    est = {"C1": 0.05, "C2": 1.7, "C2b4": 1.7, "C3": 5.0, "C5": 0.9}[args.workload] * 8 / (os.cpu_count() or 8)
+    est = {"C1": 0.05, "C2": 1.7, "C2b4": 1.7, "C2w2": 1.7, "C3": 5.0, "C5": 0.9}[args.workload] * 8 / (os.cpu_count() or 8)
     cap = max(2, int(150 / max(est, 1e-3)))
     k_run = min(steps, cap)
     gbs, ms, kind, cores, sample = cpu_reference(w, k_run, warm=min(args.warmup, 1))
