@@ -225,6 +225,26 @@ BDK_API bdk_status bdk_dequant_blocks(const bdk_cache* cache, uint32_t b, uint32
  * residual} bytes. */
 BDK_API bdk_status bdk_memory(const bdk_cache* cache, uint64_t out[4]);
 
+/* ------------------------------------------------- quant.hpp utilities */
+/* quant.hpp:56-80 on the device, host buffers in/out (synchronous).
+ * quantize_tile: x [rows][d] fp32 -> codes [rows][d] and params as (scale,
+ * zero) binary16 pairs in push order: KChannel (axis 0) [rows/g][d], KToken
+ * (axis 1) [rows][d/g] (quant.cpp:47-93); ShapeError unless g divides the
+ * grouped extent.  dequantize_tile rounds every value to binary16 storage
+ * (quant.cpp:95-110); dequantize_group does not (quant.cpp:40-44). */
+BDK_API bdk_status bdk_quantize_tile(const float* x, uint32_t rows, uint32_t d, uint32_t num_bits,
+                                     uint32_t axis, uint32_t group_size, uint16_t* codes,
+                                     uint16_t* params, int32_t device);
+BDK_API bdk_status bdk_dequantize_tile(const uint16_t* codes, const uint16_t* params,
+                                       uint32_t rows, uint32_t d, uint32_t axis,
+                                       uint32_t group_size, float* out, int32_t device);
+BDK_API bdk_status bdk_compute_group_params(const float* x, uint32_t n, uint32_t num_bits,
+                                            float* scale, float* zero, int32_t device);
+BDK_API bdk_status bdk_quantize_group(const float* x, uint32_t n, float scale, float zero,
+                                      uint32_t num_bits, uint16_t* codes, int32_t device);
+BDK_API bdk_status bdk_dequantize_group(const uint16_t* codes, uint32_t n, float scale,
+                                        float zero, float* values, int32_t device);
+
 /* ------------------------------------------------ BDKV v1 cache files */
 /* dump_cache / load_cache (serialize.hpp:11-23, serialize.cpp:87-194): the
  * reference's byte format.  bdk_dump_cache writes into buf (capacity bytes)

@@ -16,6 +16,7 @@
 // the reference grows host vectors) and a CUDA device ordinal.
 #pragma once
 
+#include <array>
 #include <bit>
 #include <cmath>
 #include <utility>
@@ -170,12 +171,136 @@ struct QuantParams {  // quant.hpp:38-47: (scale, zero) binary16 pairs
   size_t group_count() const { return rows * cols; }
   float scale(size_t g) const { return f16_bits_to_f32(data[2 * g]); }
   float zero(size_t g) const { return f16_bits_to_f32(data[2 * g + 1]); }
+  void push(float scale, float zero) {
+    data.push_back(f32_to_f16_bits(scale));
+    data.push_back(f32_to_f16_bits(zero));
+  }
   bool operator==(const QuantParams&) const = default;
 };
 
 inline constexpr float kMinScale = 6.103515625e-05f;  // quant.hpp:52
 
+// ----------------------------------------------------------- quant.hpp
+// quant.hpp:45-80 on the device (bdk_quantize_tile & co.), same values.
+struct GroupParams {
+  float scale;
+  float zero;
+};
+struct QuantizedTile {  // quant.hpp:62-65
+  std::vector<uint16_t> codes;
+  QuantParams params;
+};
+
+inline GroupParams compute_group_params(std::span<const float> group, uint32_t num_bits,
+                                        int device = 0) {
+  GroupParams g{};
+  detail::check(bdk_compute_group_params(group.data(), static_cast<uint32_t>(group.size()),
+                                         num_bits, &g.scale, &g.zero, device));
+  return g;
+}
+
+inline void quantize_group(std::span<const float> group, float scale, float zero,
+                           uint32_t num_bits, std::span<uint16_t> codes_out, int device = 0) {
+  detail::check(bdk_quantize_group(group.data(), static_cast<uint32_t>(group.size()), scale, zero,
+                                   num_bits, codes_out.data(), device));
+}
+
+inline void dequantize_group(std::span<const uint16_t> codes, float scale, float zero,
+                             std::span<float> values_out, int device = 0) {
+  detail::check(bdk_dequantize_group(codes.data(), static_cast<uint32_t>(codes.size()), scale,
+                                     zero, values_out.data(), device));
+}
+
+inline QuantizedTile quantize_tile(const float* tile, size_t rows, size_t d, uint32_t num_bits,
+                                   QuantAxis axis, size_t group_size, int device = 0) {
+  QuantizedTile out;
+  out.codes.assign(rows * d, 0);
+  const size_t groups = group_size ? rows * d / group_size : 0;
+  out.params.data.assign(2 * groups, 0);
+  detail::check(bdk_quantize_tile(tile, static_cast<uint32_t>(rows), static_cast<uint32_t>(d),
+                                  num_bits, static_cast<uint32_t>(axis),
+                                  static_cast<uint32_t>(group_size), out.codes.data(),
+                                  out.params.data.data(), device));
+  out.params.rows = axis == QuantAxis::KChannel ? rows / group_size : rows;
+  out.params.cols = axis == QuantAxis::KChannel ? d : d / group_size;
+  return out;
+}
+
+inline void dequantize_tile(const std::vector<uint16_t>& codes, const QuantParams& params,
+                            size_t rows, size_t d, QuantAxis axis, size_t group_size, float* out,
+                            int device = 0) {
+  if (codes.size() != rows * d) throw ShapeError("dequantize_tile: codes do not cover the tile");
+  detail::check(bdk_dequantize_tile(codes.data(), params.data.data(), static_cast<uint32_t>(rows),
+                                    static_cast<uint32_t>(d), static_cast<uint32_t>(axis),
+                                    static_cast<uint32_t>(group_size), out, device));
+}
+
 // ------------------------------------------------------------ layout.hpp
+// ---------------------------------------------------------- layout.hpp
+// Word-layout metadata (which field holds which element): integer helpers
+// mirroring layout.cpp:21-86 and kvcache.cpp:79-112, the layout contract the
+// device cache keeps byte-identical.
+struct InterleavePerm {  // layout.hpp:13-24
+  uint32_t num_bits = 0;
+  uint32_t pack_num = 0;
+  std::array<uint8_t, 8> order{};
+  std::array<uint8_t, 8> inverse() const {
+    std::array<uint8_t, 8> inv{};
+    for (uint32_t k = 0; k < pack_num; ++k) inv[order[k]] = static_cast<uint8_t>(k);
+    return inv;
+  }
+};
+
+namespace detail {
+inline uint32_t pack_num_of(uint32_t num_bits) {
+  if (num_bits != 2 && num_bits != 4 && num_bits != 8 && num_bits != 16)
+    throw UnsupportedBits("num_bits must be one of 2, 4, 8, 16");
+  return 16 / num_bits;
+}
+}  // namespace detail
+
+inline InterleavePerm interleave_order(uint32_t num_bits) {  // layout.cpp:21-34
+  InterleavePerm p{num_bits, detail::pack_num_of(num_bits), {}};
+  uint32_t k = 0;
+  for (int i = (int)p.pack_num - 1; i >= 0; --i)
+    if (i % 2 == 1) p.order[k++] = static_cast<uint8_t>(i);
+  for (int i = (int)p.pack_num - 1; i >= 0; --i)
+    if (i % 2 == 0) p.order[k++] = static_cast<uint8_t>(i);
+  return p;
+}
+
+inline InterleavePerm identity_order(uint32_t num_bits) {  // layout.cpp:36-43
+  InterleavePerm p{num_bits, detail::pack_num_of(num_bits), {}};
+  for (uint32_t k = 0; k < p.pack_num; ++k) p.order[k] = static_cast<uint8_t>(k);
+  return p;
+}
+
+inline uint16_t pack_word(std::span<const uint16_t> codes, const InterleavePerm& perm) {
+  uint32_t w = 0;  // layout.cpp:45-61: field k (from the MSB) holds codes[order[k]]
+  for (uint32_t k = 0; k < perm.pack_num; ++k) {
+    const uint32_t c = codes[perm.order[k]];
+    if (perm.num_bits < 16 && (c >> perm.num_bits) != 0)
+      throw CodeOverflow("pack_word: code does not fit in num_bits");
+    w |= c << (16 - (k + 1) * perm.num_bits);
+  }
+  return static_cast<uint16_t>(w);
+}
+
+inline void unpack_word(uint16_t word, const InterleavePerm& perm,
+                        std::span<uint16_t> codes_out) {  // layout.cpp:63-72
+  const uint32_t mask = perm.num_bits == 16 ? 0xFFFFu : ((1u << perm.num_bits) - 1u);
+  for (uint32_t k = 0; k < perm.pack_num; ++k)
+    codes_out[perm.order[k]] = static_cast<uint16_t>((word >> (16 - (k + 1) * perm.num_bits)) & mask);
+}
+
+inline size_t iteration_count(size_t tile_n, size_t warp_n) {  // layout.cpp:79-86
+  const size_t stride = warp_n * 8;
+  if (stride == 0 || tile_n % stride != 0) throw ShapeError("tile_n must be a multiple of warp_n*8");
+  return tile_n / stride;
+}
+
+inline size_t swizzle_col(size_t row, size_t col) { return row ^ col; }  // layout.hpp:49
+
 inline size_t residual_block_size(uint32_t num_bits, size_t warp_n) {  // layout.cpp:74-77
   if (num_bits != 2 && num_bits != 4 && num_bits != 8 && num_bits != 16)
     throw UnsupportedBits("num_bits must be one of 2, 4, 8, 16");
@@ -502,6 +627,35 @@ inline AttnOutput decode_step(KVCache& cache, const AttentionConfig& cfg, const 
   detail::check(bdk_decode_step_host(cache.handle(), &c, q.data(), k_new.data(), v_new.data(),
                                      out.data.data()));
   return out;
+}
+
+// kvcache.hpp:199-205: row-major [n_r, d] codes <-> channel-major words,
+// pack_num consecutive tokens per word
+inline std::vector<uint16_t> pack_block_codes(const std::vector<uint16_t>& codes, size_t n_r,
+                                              size_t d, const InterleavePerm& perm) {
+  if (codes.size() != n_r * d) throw ShapeError("pack_block_codes: codes do not cover block");
+  if (n_r % perm.pack_num != 0) throw ShapeError("pack_block_codes: N_r not pack-aligned");
+  const size_t groups = n_r / perm.pack_num;
+  std::vector<uint16_t> words(groups * d), tmp(perm.pack_num);
+  for (size_t c = 0; c < d; ++c)
+    for (size_t g = 0; g < groups; ++g) {
+      for (size_t k = 0; k < perm.pack_num; ++k) tmp[k] = codes[(g * perm.pack_num + k) * d + c];
+      words[c * groups + g] = pack_word(tmp, perm);
+    }
+  return words;
+}
+
+inline std::vector<uint16_t> unpack_block_codes(const std::vector<uint16_t>& words, size_t n_r,
+                                                size_t d, const InterleavePerm& perm) {
+  const size_t groups = n_r / perm.pack_num;
+  if (words.size() != groups * d) throw ShapeError("unpack_block_codes: word count mismatch");
+  std::vector<uint16_t> codes(n_r * d), tmp(perm.pack_num);
+  for (size_t c = 0; c < d; ++c)
+    for (size_t g = 0; g < groups; ++g) {
+      unpack_word(words[c * groups + g], perm, tmp);
+      for (size_t k = 0; k < perm.pack_num; ++k) codes[(g * perm.pack_num + k) * d + c] = tmp[k];
+    }
+  return codes;
 }
 
 // ------------------------------------------------------------ serialize.hpp

@@ -47,6 +47,11 @@ SIGNATURES = {
     "bdk_prefill": (C.c_int, [vp, u32, u32, vp, vp, u32, vp]),
     "bdk_prefill_all": (C.c_int, [vp, vp, vp, u32, vp]),
     "bdk_cache_reset": (C.c_int, [vp, vp]),
+    "bdk_quantize_tile": (C.c_int, [vp, u32, u32, u32, u32, u32, vp, vp, i32]),
+    "bdk_dequantize_tile": (C.c_int, [vp, vp, u32, u32, u32, u32, vp, i32]),
+    "bdk_compute_group_params": (C.c_int, [vp, u32, u32, fp, fp, i32]),
+    "bdk_quantize_group": (C.c_int, [vp, u32, C.c_float, C.c_float, u32, vp, i32]),
+    "bdk_dequantize_group": (C.c_int, [vp, u32, C.c_float, C.c_float, vp, i32]),
     "bdk_peer_merge": (C.c_int, [C.POINTER(vp), C.POINTER(vp), u32, u32, C.c_uint64, u32, u32, vp,
                                  vp, vp, C.c_uint64, vp]),
     "bdk_dump_cache": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(C.c_uint64)]),

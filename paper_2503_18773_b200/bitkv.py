@@ -157,6 +157,170 @@ def residual_block_size(num_bits: int, warp_n: int) -> int:
 
 
 # --------------------------------------------------------------- kvcache.hpp
+# ----------------------------------------------------------- quant.hpp API
+@dataclass
+class GroupParams:
+    """quant.hpp:45-48"""
+    scale: float
+    zero: float
+
+
+@dataclass
+class QuantParams:
+    """quant.hpp:30-43: (scale, zero) binary16 bit pairs, grid rows x cols."""
+    rows: int
+    cols: int
+    data: np.ndarray  # uint16 [2 * rows * cols]
+
+    def group_count(self) -> int:
+        return self.rows * self.cols
+
+    def scale(self, g: int) -> float:
+        return float(self.data[2 * g:2 * g + 1].view(np.float16)[0])
+
+    def zero(self, g: int) -> float:
+        return float(self.data[2 * g + 1:2 * g + 2].view(np.float16)[0])
+
+
+@dataclass
+class QuantizedTile:
+    """quant.hpp:62-65: row-major [rows, d] codes + params."""
+    codes: np.ndarray  # uint16 [rows, d]
+    params: QuantParams
+
+
+def compute_group_params(group, num_bits: int, device: int = 0) -> GroupParams:
+    """compute_group_params (quant.cpp:18-28), on the device."""
+    x = np.ascontiguousarray(group, np.float32).ravel()
+    s, z = C.c_float(), C.c_float()
+    _check(_L.load().bdk_compute_group_params(x.ctypes.data, x.size, num_bits, C.byref(s),
+                                              C.byref(z), device))
+    return GroupParams(s.value, z.value)
+
+
+def quantize_group(group, scale: float, zero: float, num_bits: int, device: int = 0) -> np.ndarray:
+    """quantize_group (quant.cpp:30-38), on the device -> uint16 codes."""
+    x = np.ascontiguousarray(group, np.float32).ravel()
+    codes = np.zeros(x.size, np.uint16)
+    _check(_L.load().bdk_quantize_group(x.ctypes.data, x.size, scale, zero, num_bits,
+                                        codes.ctypes.data, device))
+    return codes
+
+
+def dequantize_group(codes, scale: float, zero: float, device: int = 0) -> np.ndarray:
+    """dequantize_group (quant.cpp:40-44): code * scale + zero in fp32."""
+    c = np.ascontiguousarray(codes, np.uint16).ravel()
+    out = np.zeros(c.size, np.float32)
+    _check(_L.load().bdk_dequantize_group(c.ctypes.data, c.size, scale, zero, out.ctypes.data,
+                                          device))
+    return out
+
+
+def quantize_tile(tile, num_bits: int, axis: QuantAxis, group_size: int,
+                  device: int = 0) -> QuantizedTile:
+    """quantize_tile (quant.cpp:47-93) of a row-major [rows, d] tile."""
+    x = np.ascontiguousarray(tile, np.float32)
+    rows, d = x.shape
+    codes = np.zeros((rows, d), np.uint16)
+    groups = rows * d // group_size if group_size else 0
+    prm = np.zeros(2 * max(groups, 1), np.uint16)
+    _check(_L.load().bdk_quantize_tile(x.ctypes.data, rows, d, num_bits, int(axis), group_size,
+                                       codes.ctypes.data, prm.ctypes.data, device))
+    pr, pc = ((rows // group_size, d) if QuantAxis(axis) == QuantAxis.KChannel
+              else (rows, d // group_size))
+    return QuantizedTile(codes, QuantParams(pr, pc, prm[:2 * groups]))
+
+
+def dequantize_tile(codes, params: QuantParams, rows: int, d: int, axis: QuantAxis,
+                    group_size: int, device: int = 0) -> np.ndarray:
+    """dequantize_tile (quant.cpp:95-110): values rounded to binary16."""
+    c = np.ascontiguousarray(codes, np.uint16)
+    if c.size != rows * d:
+        raise ShapeError("dequantize_tile: codes do not cover the tile")
+    prm = np.ascontiguousarray(params.data, np.uint16)
+    out = np.zeros((rows, d), np.float32)
+    _check(_L.load().bdk_dequantize_tile(c.ctypes.data, prm.ctypes.data, rows, d, int(axis),
+                                         group_size, out.ctypes.data, device))
+    return out
+
+
+# ---------------------------------------------------------- layout.hpp API
+# The word layout is metadata (which field holds which token), not
+# arithmetic: these mirror layout.cpp:21-86 for callers of the reference API.
+def interleave_order(num_bits: int) -> list[int]:
+    """interleave_order (layout.cpp:21-34): odd indices descending, then even."""
+    p = _pack_num(num_bits)
+    return [i for i in range(p - 1, -1, -1) if i % 2] + [i for i in range(p - 1, -1, -1)
+                                                        if i % 2 == 0]
+
+
+def identity_order(num_bits: int) -> list[int]:
+    """identity_order (layout.cpp:36-43)."""
+    return list(range(_pack_num(num_bits)))
+
+
+def _pack_num(num_bits: int) -> int:
+    if num_bits not in (2, 4, 8, 16):
+        raise UnsupportedBits(f"num_bits must be one of 2, 4, 8, 16, got {num_bits}")
+    return 16 // num_bits
+
+
+def pack_word(codes, num_bits: int, order: list[int]) -> int:
+    """pack_word (layout.cpp:45-61): field k (from the MSB) holds codes[order[k]];
+    CodeOverflow if a code needs more than num_bits bits."""
+    p = _pack_num(num_bits)
+    w = 0
+    for k in range(p):
+        c = int(codes[order[k]])
+        if c >> num_bits:
+            raise CodeOverflow(f"code {c} does not fit in {num_bits} bits")
+        w |= c << (16 - (k + 1) * num_bits)
+    return w
+
+
+def unpack_word(word: int, num_bits: int, order: list[int]) -> list[int]:
+    """unpack_word (layout.cpp:63-72)."""
+    p = _pack_num(num_bits)
+    out = [0] * p
+    for k in range(p):
+        out[order[k]] = (word >> (16 - (k + 1) * num_bits)) & ((1 << num_bits) - 1)
+    return out
+
+
+def pack_block_codes(codes, n_r: int, d: int, num_bits: int, order: list[int]) -> np.ndarray:
+    """pack_block_codes (kvcache.cpp:79-95): row-major [n_r, d] codes ->
+    channel-major words, pack_num consecutive tokens per word."""
+    p = _pack_num(num_bits)
+    c = np.asarray(codes, np.uint32).reshape(n_r, d)
+    if n_r % p:
+        raise ShapeError("pack_block_codes: N_r not pack-aligned")
+    if num_bits < 16 and (c >> num_bits).any():
+        raise CodeOverflow(f"a code does not fit in {num_bits} bits")
+    g = c.reshape(n_r // p, p, d)  # [word group, token in word, channel]
+    w = np.zeros((n_r // p, d), np.uint32)
+    for k in range(p):
+        w |= g[:, order[k], :] << (16 - (k + 1) * num_bits)
+    return w.T.reshape(-1).astype(np.uint16)  # [d][n_r / p]
+
+
+def unpack_block_codes(words, n_r: int, d: int, num_bits: int, order: list[int]) -> np.ndarray:
+    """unpack_block_codes (kvcache.cpp:97-112)."""
+    p = _pack_num(num_bits)
+    w = np.asarray(words, np.uint32).reshape(d, n_r // p).T  # [word group, channel]
+    mask = (1 << num_bits) - 1 if num_bits < 16 else 0xFFFF
+    out = np.zeros((n_r // p, p, d), np.uint16)
+    for k in range(p):
+        out[:, order[k], :] = (w >> (16 - (k + 1) * num_bits)) & mask
+    return out.reshape(n_r, d)
+
+
+def iteration_count(tile_n: int, warp_n: int) -> int:
+    """iteration_count (layout.cpp:79-86): T_n / (W_n * 8)."""
+    if warp_n == 0 or tile_n % (warp_n * 8):
+        raise ShapeError(f"tile_n ({tile_n}) must be a multiple of warp_n * 8")
+    return tile_n // (warp_n * 8)
+
+
 @dataclass
 class PackedBlock:
     """kvcache.hpp:17-26 (u16 arrays in the reference layout)."""

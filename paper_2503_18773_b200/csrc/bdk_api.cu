@@ -1314,4 +1314,127 @@ bdk_status bdk_load_cache_file(const char* path, uint32_t max_tokens, int32_t de
   return bdk_load_cache(data.data(), data.size(), max_tokens, device, out);
 }
 
+
+// ------------------------------------------------- quant.hpp utilities
+// quantize_tile / dequantize_tile / compute_group_params / quantize_group /
+// dequantize_group (quant.hpp:56-80) on the device: host buffers in and out,
+// synchronous.  Same validation and error classes as the reference.
+namespace {
+struct DevBuf {  // scoped device allocation
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+bdk_status quant_common(uint32_t bits, int32_t device) {
+  if (bits == 0 || bits > 16) return fail(BDK_UNSUPPORTED_BITS, "num_bits must be 1..16");
+  BDK_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  return BDK_OK;
+}
+}  // namespace
+
+bdk_status bdk_quantize_tile(const float* x, uint32_t rows, uint32_t d, uint32_t bits,
+                             uint32_t axis, uint32_t group_size, uint16_t* codes,
+                             uint16_t* params, int32_t device) {
+  if (!x || !codes || !params) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  if (axis > 1) return fail(BDK_CONFIG_ERROR, "axis must be 0 (KChannel) or 1 (KToken)");
+  const uint32_t extent = axis == 0 ? rows : d;
+  if (group_size == 0 || extent % group_size != 0)
+    return fail(BDK_SHAPE_ERROR, "group_size (" + std::to_string(group_size) +
+                                     ") must divide the grouped extent (" +
+                                     std::to_string(extent) + ")");
+  bdk_status s = quant_common(bits, device);
+  if (s) return s;
+  const size_t n = (size_t)rows * d;
+  const size_t groups = n / group_size;
+  if (n == 0) return BDK_OK;
+  DevBuf bx, bc, bp;
+  BDK_CUDA(cudaMalloc(&bx.p, n * 4), "cudaMalloc");
+  BDK_CUDA(cudaMalloc(&bc.p, n * 2), "cudaMalloc");
+  BDK_CUDA(cudaMalloc(&bp.p, groups * 4), "cudaMalloc");
+  BDK_CUDA(cudaMemcpy(bx.p, x, n * 4, cudaMemcpyHostToDevice), "H2D");
+  BDK_CUDA(bdk::launch_quantize_tile(static_cast<float*>(bx.p), (int)rows, (int)d, (int)bits,
+                                     (int)axis, (int)group_size, static_cast<uint16_t*>(bc.p),
+                                     static_cast<uint32_t*>(bp.p), nullptr),
+           "quantize_tile launch");
+  BDK_CUDA(cudaMemcpy(codes, bc.p, n * 2, cudaMemcpyDeviceToHost), "D2H codes");
+  BDK_CUDA(cudaMemcpy(params, bp.p, groups * 4, cudaMemcpyDeviceToHost), "D2H params");
+  return BDK_OK;
+}
+
+bdk_status bdk_dequantize_tile(const uint16_t* codes, const uint16_t* params, uint32_t rows,
+                               uint32_t d, uint32_t axis, uint32_t group_size, float* out,
+                               int32_t device) {
+  if (!codes || !params || !out) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  if (axis > 1) return fail(BDK_CONFIG_ERROR, "axis must be 0 (KChannel) or 1 (KToken)");
+  const uint32_t extent = axis == 0 ? rows : d;
+  if (group_size == 0 || extent % group_size != 0)
+    return fail(BDK_SHAPE_ERROR, "dequantize_tile: group_size must divide the grouped extent");
+  BDK_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  const size_t n = (size_t)rows * d;
+  const size_t groups = n / group_size;
+  if (n == 0) return BDK_OK;
+  DevBuf bc, bp, bo;
+  BDK_CUDA(cudaMalloc(&bc.p, n * 2), "cudaMalloc");
+  BDK_CUDA(cudaMalloc(&bp.p, groups * 4), "cudaMalloc");
+  BDK_CUDA(cudaMalloc(&bo.p, n * 4), "cudaMalloc");
+  BDK_CUDA(cudaMemcpy(bc.p, codes, n * 2, cudaMemcpyHostToDevice), "H2D");
+  BDK_CUDA(cudaMemcpy(bp.p, params, groups * 4, cudaMemcpyHostToDevice), "H2D");
+  BDK_CUDA(bdk::launch_dequantize_tile(static_cast<uint16_t*>(bc.p),
+                                       static_cast<uint32_t*>(bp.p), (int)rows, (int)d, (int)axis,
+                                       (int)group_size, 1, static_cast<float*>(bo.p), nullptr),
+           "dequantize_tile launch");
+  BDK_CUDA(cudaMemcpy(out, bo.p, n * 4, cudaMemcpyDeviceToHost), "D2H");
+  return BDK_OK;
+}
+
+bdk_status bdk_compute_group_params(const float* x, uint32_t n, uint32_t bits, float* scale,
+                                    float* zero, int32_t device) {
+  if (!x || !scale || !zero) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  if (n == 0) return fail(BDK_EMPTY_INPUT, "compute_group_params: empty group");
+  std::vector<uint16_t> codes(n), prm(2);
+  bdk_status s = bdk_quantize_tile(x, n, 1, bits, 0, n, codes.data(), prm.data(), device);
+  if (s) return s;
+  __half hs, hz;
+  std::memcpy(&hs, &prm[0], 2);
+  std::memcpy(&hz, &prm[1], 2);
+  *scale = __half2float(hs);
+  *zero = __half2float(hz);
+  return BDK_OK;
+}
+
+bdk_status bdk_quantize_group(const float* x, uint32_t n, float scale, float zero, uint32_t bits,
+                              uint16_t* codes, int32_t device) {
+  if (!x || !codes) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  bdk_status s = quant_common(bits, device);
+  if (s) return s;
+  if (n == 0) return BDK_OK;
+  DevBuf bx, bc;
+  BDK_CUDA(cudaMalloc(&bx.p, (size_t)n * 4), "cudaMalloc");
+  BDK_CUDA(cudaMalloc(&bc.p, (size_t)n * 2), "cudaMalloc");
+  BDK_CUDA(cudaMemcpy(bx.p, x, (size_t)n * 4, cudaMemcpyHostToDevice), "H2D");
+  BDK_CUDA(bdk::launch_quantize_group(static_cast<float*>(bx.p), (int)n, scale, zero, (int)bits,
+                                      static_cast<uint16_t*>(bc.p), nullptr),
+           "quantize_group launch");
+  BDK_CUDA(cudaMemcpy(codes, bc.p, (size_t)n * 2, cudaMemcpyDeviceToHost), "D2H");
+  return BDK_OK;
+}
+
+bdk_status bdk_dequantize_group(const uint16_t* codes, uint32_t n, float scale, float zero,
+                                float* values, int32_t device) {
+  if (!codes || !values) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  BDK_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  if (n == 0) return BDK_OK;
+  DevBuf bc, bo;
+  BDK_CUDA(cudaMalloc(&bc.p, (size_t)n * 2), "cudaMalloc");
+  BDK_CUDA(cudaMalloc(&bo.p, (size_t)n * 4), "cudaMalloc");
+  BDK_CUDA(cudaMemcpy(bc.p, codes, (size_t)n * 2, cudaMemcpyHostToDevice), "H2D");
+  BDK_CUDA(bdk::launch_dequantize_group(static_cast<uint16_t*>(bc.p), (int)n, scale, zero,
+                                        static_cast<float*>(bo.p), nullptr),
+           "dequantize_group launch");
+  BDK_CUDA(cudaMemcpy(values, bo.p, (size_t)n * 4, cudaMemcpyDeviceToHost), "D2H");
+  return BDK_OK;
+}
+
 }  // extern "C"

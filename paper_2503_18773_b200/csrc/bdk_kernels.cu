@@ -710,6 +710,73 @@ __global__ void __launch_bounds__(128) peer_merge_kernel(PeerMergeArgs a) {
   }
 }
 
+// ------------------------------------------------- quant.hpp utilities
+// quantize_tile / dequantize_tile / compute_group_params (quant.cpp:18-110)
+// for callers of the reference's quant API: one thread per group scanning it
+// in the reference's order (strict compares keep the first extremum, so the
+// sign of a zero extremum needs no special case), the same IEEE arithmetic
+// as the packing kernels.  axis 0 = KChannel (groups along rows, params
+// [rows/g][d]), 1 = KToken (groups along d, params [rows][d/g]).
+__global__ void quantize_tile_kernel(const float* x, int rows, int d, int bits, int axis, int g,
+                                     uint16_t* codes, uint32_t* params) {
+  const int n_groups = axis == 0 ? (rows / g) * d : rows * (d / g);
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= n_groups) return;
+  // element i of group gi: KChannel group (gr, c) runs over rows gr*g..; KToken (t, gc) over cols
+  int base, stride;
+  if (axis == 0) {
+    const int gr = gi / d, c = gi % d;
+    base = gr * g * d + c;
+    stride = d;
+  } else {
+    const int t = gi / (d / g), gc = gi % (d / g);
+    base = t * d + gc * g;
+    stride = 1;
+  }
+  float lo = x[base], hi = lo;
+  for (int i = 1; i < g; ++i) {
+    const float v = x[base + i * stride];
+    lo = v < lo ? v : lo;
+    hi = hi < v ? v : hi;
+  }
+  const float qmax = static_cast<float>((1u << bits) - 1u);
+  float s, z;
+  group_params(lo, hi, qmax, s, z);
+  params[gi] = param_u32(s, z);
+  for (int i = 0; i < g; ++i)
+    codes[base + i * stride] = static_cast<uint16_t>(quant_code(x[base + i * stride], s, z, qmax));
+}
+
+// out = round_f16(code * scale + zero), the product and sum each rounded in
+// fp32 like the reference's non-contracted `code * scale + zero`
+__global__ void dequantize_tile_kernel(const uint16_t* codes, const uint32_t* params, int rows,
+                                       int d, int axis, int g, int round16, float* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * d) return;
+  const int t = i / d, c = i % d;
+  const int gi = axis == 0 ? (t / g) * d + c : t * (d / g) + c / g;
+  const uint32_t p = params[gi];
+  const float s = __half2float(__ushort_as_half(static_cast<unsigned short>(p & 0xFFFF)));
+  const float z = __half2float(__ushort_as_half(static_cast<unsigned short>(p >> 16)));
+  const float v = __fadd_rn(__fmul_rn(static_cast<float>(codes[i]), s), z);
+  out[i] = round16 ? __half2float(__float2half_rn(v)) : v;
+}
+
+// quantize_group / dequantize_group (quant.cpp:30-44) with explicit fp32
+// (scale, zero): codes as quantize_tile, values in fp32 without rounding
+__global__ void quantize_group_kernel(const float* x, int n, float s, float z, int bits,
+                                      uint16_t* codes) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n)
+    codes[i] = static_cast<uint16_t>(quant_code(x[i], s, z, static_cast<float>((1u << bits) - 1u)));
+}
+
+__global__ void dequantize_group_kernel(const uint16_t* codes, int n, float s, float z,
+                                        float* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __fadd_rn(__fmul_rn(static_cast<float>(codes[i]), s), z);
+}
+
 // ------------------------------------------------------------- launchers
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device,
@@ -900,6 +967,33 @@ cudaError_t launch_merge_partials(const float* o, const float* lse, int n_parts,
 cudaError_t launch_peer_merge(const PeerMergeArgs& a, cudaStream_t s) {
   const int grid = std::max(1, std::min(a.rows, 16));  // few CTAs: never crowd out a peer
   peer_merge_kernel<<<grid, 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quantize_tile(const float* x, int rows, int d, int bits, int axis, int g,
+                                 uint16_t* codes, uint32_t* params, cudaStream_t s) {
+  const int n_groups = axis == 0 ? (rows / g) * d : rows * (d / g);
+  quantize_tile_kernel<<<(n_groups + 127) / 128, 128, 0, s>>>(x, rows, d, bits, axis, g, codes,
+                                                              params);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize_tile(const uint16_t* codes, const uint32_t* params, int rows, int d,
+                                   int axis, int g, int round16, float* out, cudaStream_t s) {
+  dequantize_tile_kernel<<<(rows * d + 255) / 256, 256, 0, s>>>(codes, params, rows, d, axis, g,
+                                                                round16, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quantize_group(const float* x, int n, float s, float z, int bits,
+                                  uint16_t* codes, cudaStream_t st) {
+  quantize_group_kernel<<<(n + 255) / 256, 256, 0, st>>>(x, n, s, z, bits, codes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize_group(const uint16_t* codes, int n, float s, float z, float* out,
+                                    cudaStream_t st) {
+  dequantize_group_kernel<<<(n + 255) / 256, 256, 0, st>>>(codes, n, s, z, out);
   return cudaGetLastError();
 }
 

@@ -110,6 +110,17 @@ struct PeerMergeArgs {
 };
 cudaError_t launch_peer_merge(const PeerMergeArgs& a, cudaStream_t s);
 
+// quant.hpp utilities (bdk_quantize_tile / bdk_dequantize_tile)
+cudaError_t launch_quantize_tile(const float* x, int rows, int d, int bits, int axis, int g,
+                                 uint16_t* codes, uint32_t* params, cudaStream_t s);
+cudaError_t launch_dequantize_tile(const uint16_t* codes, const uint32_t* params, int rows, int d,
+                                   int axis, int g, int round16, float* out, cudaStream_t s);
+
+cudaError_t launch_quantize_group(const float* x, int n, float s, float z, int bits,
+                                  uint16_t* codes, cudaStream_t st);
+cudaError_t launch_dequantize_group(const uint16_t* codes, int n, float s, float z, float* out,
+                                    cudaStream_t st);
+
 cudaError_t launch_merge_partials(const float* o, const float* lse, int n_parts, int rows, int d,
                                   size_t o_stride, size_t lse_stride, float* out, cudaStream_t s);
 

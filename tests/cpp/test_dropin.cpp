@@ -210,6 +210,39 @@ static void serialize_round_trip(uint32_t bits) {
   }
 }
 
+// layout.hpp / quant.hpp API of the drop-in (test_layout.cpp:13-39,
+// test_quant.cpp:27-69)
+static void quant_and_layout_api() {
+  const InterleavePerm p2 = interleave_order(2);
+  const uint8_t want2[8] = {7, 5, 3, 1, 6, 4, 2, 0};
+  CHECK(std::memcmp(p2.order.data(), want2, 8) == 0);
+  const uint16_t c4[4] = {1, 2, 3, 4};
+  CHECK(pack_word(c4, interleave_order(4)) == 0x4231);
+  uint16_t back[4] = {};
+  unpack_word(0x4231, interleave_order(4), back);
+  CHECK(std::memcmp(back, c4, 8) == 0);
+  const uint16_t big[4] = {16, 0, 0, 0};
+  CHECK(throws_as<CodeOverflow>([&] { pack_word(big, interleave_order(4)); }));
+  const float g[4] = {-1.f, 0.f, 2.f, 5.f};
+  uint16_t codes[4] = {};
+  quantize_group(g, 0.4f, -1.0f, 4, codes);  // round half to even: {0, 2, 8, 15}
+  CHECK(codes[0] == 0 && codes[1] == 2 && codes[2] == 8 && codes[3] == 15);
+  const GroupParams gp = compute_group_params(g, 4);
+  CHECK(gp.zero == -1.0f && gp.scale == round_f16(6.0f / 15.0f));
+  // quantize_tile -> pack_block_codes == the cache's own packed block
+  const size_t d = 128, n_r = 128;
+  orc_gauss rng;
+  orc_gauss_init(&rng, 77);
+  const auto k = gauss(rng, n_r * d), v = gauss(rng, n_r * d);
+  KVCache cache(1, 1, d, 4, QuantSpec{4, QuantAxis::KChannel, 128});
+  cache.prefill(0, 0, k.data(), v.data(), n_r);
+  const PackedBlock blk = cache.packed(0, 0).blocks.at(0);
+  const QuantizedTile qk = quantize_tile(k.data(), n_r, d, 4, QuantAxis::KChannel, 128);
+  CHECK(pack_block_codes(qk.codes, n_r, d, interleave_order(4)) == blk.k_words);
+  CHECK(qk.params.data == blk.k_params.data);
+  CHECK(unpack_block_codes(blk.k_words, n_r, d, interleave_order(4)) == qk.codes);
+}
+
 int main() {
   prefill_is_bit_exact(4, 4, 128, QuantAxis::KChannel);
   prefill_is_bit_exact(2, 4, 128, QuantAxis::KChannel);
@@ -222,6 +255,7 @@ int main() {
   errors_map_to_reference_exceptions();
   serialize_round_trip(4);
   serialize_round_trip(2);
+  quant_and_layout_api();
   std::printf("%s: %d failed checks\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail;
 }
