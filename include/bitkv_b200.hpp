@@ -416,6 +416,10 @@ class KVCache {  // kvcache.hpp:103-189, cache resident in HBM
   CacheBackend backend() const { return backend_; }
   size_t page_size() const { return page_size_; }
   bool interleaved() const { return interleave_; }
+  // KVCache::perm (kvcache.hpp:120): the word permutation of this cache
+  InterleavePerm perm() const {
+    return interleave_ ? interleave_order(spec_.num_bits) : identity_order(spec_.num_bits);
+  }
   bdk_cache* handle() const { return h_; }
 
   // KVCache::prefill (kvcache.cpp:155-168): fused quantize+pack on device
