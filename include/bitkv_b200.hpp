@@ -135,6 +135,7 @@ class Tensor {  // tensor.hpp:16-81: row-major fp32 storage of binary16 values
   void set(size_t i, size_t j, size_t k, float v) { data_[flat3(i, j, k)] = round_f16(v); }
   const float* data() const { return data_.data(); }
   const std::vector<float>& values() const { return data_; }
+  bool same_elements(const Tensor& other) const { return data_ == other.data_; }  // tensor.hpp:62
 
  private:
   static size_t count(const std::vector<size_t>& s) {
@@ -337,6 +338,32 @@ inline bdk_attn_config to_c(const AttentionConfig& c) {
 }
 }  // namespace detail
 
+// gqa_transform / gqa_untransform (config.hpp:31-38, config.cpp:32-68):
+// regroup the query heads sharing a KV head, [1, heads_q, d] <->
+// [n_group, heads_kv, d]; a pure element permutation
+inline Tensor gqa_transform(const Tensor& q, size_t n_group) {
+  if (q.ndim() != 3 || q.dim(0) != 1) throw ShapeError("gqa_transform expects shape [1, heads_q, d]");
+  const size_t heads_q = q.dim(1), d = q.dim(2);
+  if (n_group == 0 || heads_q % n_group != 0) throw ShapeError("heads_q must be divisible by n_group");
+  const size_t heads_kv = heads_q / n_group;
+  Tensor out({n_group, heads_kv, d});
+  for (size_t h = 0; h < heads_kv; ++h)
+    for (size_t g = 0; g < n_group; ++g)
+      for (size_t k = 0; k < d; ++k) out.set(g, h, k, q(0, h * n_group + g, k));
+  return out;
+}
+
+inline Tensor gqa_untransform(const Tensor& q, size_t n_group) {
+  if (q.ndim() != 3 || q.dim(0) != n_group)
+    throw ShapeError("gqa_untransform expects shape [n_group, heads_kv, d]");
+  const size_t heads_kv = q.dim(1), d = q.dim(2);
+  Tensor out({1, heads_kv * n_group, d});
+  for (size_t h = 0; h < heads_kv; ++h)
+    for (size_t g = 0; g < n_group; ++g)
+      for (size_t k = 0; k < d; ++k) out.set(size_t{0}, h * n_group + g, k, q(g, h, k));
+  return out;
+}
+
 inline AttentionConfig validate_config(const AttentionConfig& cfg) {  // config.cpp:10-30
   const bdk_attn_config c = detail::to_c(cfg);
   detail::check(bdk_validate_config(&c));
@@ -355,7 +382,97 @@ struct PackedBlock {  // kvcache.hpp:17-26
 struct PackedKV {  // kvcache.hpp:28-43
   std::vector<PackedBlock> blocks;
   size_t packed_len = 0;
+  size_t k_word_count() const {
+    size_t n = 0;
+    for (const auto& b : blocks) n += b.k_words.size();
+    return n;
+  }
+  size_t v_word_count() const {
+    size_t n = 0;
+    for (const auto& b : blocks) n += b.v_words.size();
+    return n;
+  }
 };
+
+struct ResidualCache {  // kvcache.hpp:45-50 (host view of a residual window)
+  std::vector<float> k;
+  std::vector<float> v;
+  size_t res_len = 0;
+};
+
+// ---- paged residual bookkeeping (kvcache.hpp:52-97): host-side token pages
+// for callers that manage their own residual tails.  The device cache keeps
+// its residual window contiguous in HBM (CacheBackend::Paged is accepted and
+// observationally identical, test_kvcache.cpp:243-283).
+class PagePool {
+ public:
+  PagePool() = default;
+  PagePool(size_t page_size, size_t head_dim, size_t max_pages = 0)
+      : page_size_(page_size), head_dim_(head_dim), max_pages_(max_pages) {}
+
+  // a recycled page first (most recently released), else a new one;
+  // CapacityError once max_pages pages exist and none is free
+  uint32_t alloc() {
+    if (!free_.empty()) {
+      const uint32_t id = free_.back();
+      free_.pop_back();
+      return id;
+    }
+    if (max_pages_ && k_.size() >= max_pages_) throw CapacityError("page pool exhausted");
+    k_.emplace_back(page_size_ * head_dim_, 0.0f);
+    v_.emplace_back(page_size_ * head_dim_, 0.0f);
+    return static_cast<uint32_t>(k_.size() - 1);
+  }
+  void release(uint32_t id) { free_.push_back(id); }
+
+  float* k_row(uint32_t page, size_t slot) { return k_[page].data() + slot * head_dim_; }
+  float* v_row(uint32_t page, size_t slot) { return v_[page].data() + slot * head_dim_; }
+  const float* k_row(uint32_t page, size_t slot) const { return k_[page].data() + slot * head_dim_; }
+  const float* v_row(uint32_t page, size_t slot) const { return v_[page].data() + slot * head_dim_; }
+
+  size_t page_size() const { return page_size_; }
+  size_t live_pages() const { return k_.size() - free_.size(); }
+
+ private:
+  std::vector<std::vector<float>> k_, v_;
+  std::vector<uint32_t> free_;
+  size_t page_size_ = 0, head_dim_ = 0, max_pages_ = 0;
+};
+
+struct PageTable {  // logical tokens -> pool pages; pages == ceil(length / page_size)
+  size_t page_size = 16;
+  std::vector<uint32_t> pages;
+  size_t length = 0;
+};
+
+inline void paged_append(PageTable& pt, PagePool& pool, const float* k_row, const float* v_row,
+                         size_t d) {
+  const size_t slot = pt.length % pt.page_size;
+  if (slot == 0) pt.pages.push_back(pool.alloc());
+  std::memcpy(pool.k_row(pt.pages.back(), slot), k_row, d * sizeof(float));
+  std::memcpy(pool.v_row(pt.pages.back(), slot), v_row, d * sizeof(float));
+  ++pt.length;
+}
+
+inline void paged_gather(const PageTable& pt, const PagePool& pool, size_t t0, size_t len,
+                         size_t d, float* k_out, float* v_out) {
+  if (t0 + len > pt.length) throw ShapeError("paged_gather: range past end of table");
+  for (size_t i = 0; i < len; ++i) {
+    const size_t t = t0 + i;
+    const uint32_t page = pt.pages[t / pt.page_size];
+    std::memcpy(k_out + i * d, pool.k_row(page, t % pt.page_size), d * sizeof(float));
+    std::memcpy(v_out + i * d, pool.v_row(page, t % pt.page_size), d * sizeof(float));
+  }
+}
+
+inline void paged_pop_front(PageTable& pt, PagePool& pool, size_t n_tokens) {
+  if (n_tokens > pt.length) throw StateError("paged_pop_front: more tokens than resident");
+  if (n_tokens % pt.page_size != 0) throw StateError("paged_pop_front: must drop whole pages");
+  const size_t n = n_tokens / pt.page_size;
+  for (size_t i = 0; i < n; ++i) pool.release(pt.pages[i]);
+  pt.pages.erase(pt.pages.begin(), pt.pages.begin() + static_cast<std::ptrdiff_t>(n));
+  pt.length -= n_tokens;
+}
 
 enum class CacheBackend { Contiguous, Paged };  // kvcache.hpp:100
 
@@ -401,6 +518,7 @@ class KVCache {  // kvcache.hpp:103-189, cache resident in HBM
     page_size_ = o.page_size_;
     interleave_ = o.interleave_;
     info_ = o.info_;
+    snap_ = std::move(o.snap_);
     return *this;
   }
   ~KVCache() {
@@ -462,12 +580,18 @@ class KVCache {  // kvcache.hpp:103-189, cache resident in HBM
     return l.first + l.second;
   }
 
-  // KVCache::packed(b, h) (kvcache.hpp:148): host copy of the packed segment
-  PackedKV packed(size_t b, size_t h) const {
-    PackedKV out;
+  // KVCache::packed(b, h) (kvcache.hpp:148). The segment lives in HBM; this
+  // refreshes a per-cell host snapshot and returns a reference to it, so the
+  // reference's `const PackedBlock& blk = cache.packed(b, h).blocks[0];`
+  // stays valid until the next packed(b, h) call on the same cell.
+  const PackedKV& packed(size_t b, size_t h) const {
+    if (b >= batch_ || h >= heads_kv_) throw ConfigError("packed: cell out of range");
+    if (snap_.size() != batch_ * heads_kv_) snap_.assign(batch_ * heads_kv_, PackedKV{});
+    PackedKV& out = snap_[b * heads_kv_ + h];
     out.packed_len = packed_len(b, h);
     const size_t nb = out.packed_len / n_r();
-    for (size_t i = 0; i < nb; ++i) out.blocks.push_back(block(b, h, i));
+    out.blocks.resize(nb);
+    for (size_t i = 0; i < nb; ++i) out.blocks[i] = block(b, h, i);
     return out;
   }
   // KVCache::build_block (kvcache.cpp:208-219): pack the full residual on the
@@ -599,6 +723,7 @@ class KVCache {  // kvcache.hpp:103-189, cache resident in HBM
   size_t page_size_ = 16;
   bool interleave_ = true;
   bdk_cache_info info_{};
+  mutable std::vector<PackedKV> snap_;  // host snapshots handed out by packed()
 };
 
 // --------------------------------------------------------- attention.hpp

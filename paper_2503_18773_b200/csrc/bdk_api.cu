@@ -161,6 +161,10 @@ bdk_status check_decode(bdk_cache* c, const bdk_attn_config* cfg, bool appends) 
     return fail(BDK_SHAPE_ERROR, "decode_step: cache geometry does not match config");
   if (cfg->heads_q / cfg->heads_kv > 8)
     return fail(BDK_UNSUPPORTED, "n_group > 8 is outside the decode kernel envelope");
+  if (!bdk::fast_path_ok(c->dev.G))
+    return fail(BDK_UNSUPPORTED,
+                "geometry outside the sm_100a decode kernels' envelope (head_dim 128, warp_n in "
+                "{1,2,4,8}, group_size % 16 == 0, channel-wise group_size % (8*16/bits) == 0)");
   if (appends) {
     const int n_r = c->dev.G.n_r;
     for (size_t i = 0; i < c->res_len.size(); ++i) {
@@ -437,10 +441,12 @@ bdk_status bdk_cache_create(const bdk_cache_desc* d, bdk_cache** out) {
   G.kp_bytes = 2 * kp;
   G.vp_bytes = 2 * vp;
   G.rec_bytes = ((2 * G.wbytes + G.kp_bytes + G.vp_bytes) + 127) / 128 * 128;
-  if (!bdk::fast_path_ok(G))
-    return fail(BDK_UNSUPPORTED,
-                "geometry outside the sm_100a kernel envelope (head_dim 128, warp_n in "
-                "{1,2,4,8}, group_size % 16 == 0, channel-wise group_size % (8*16/bits) == 0)");
+  // any geometry the reference accepts can be stored, prefilled, flushed,
+  // read back and serialized; only decode needs the attention kernels'
+  // envelope (checked in check_decode).  The chunk swizzle needs a
+  // power-of-two warp_n.
+  if (d->warp_n & (d->warp_n - 1))
+    return fail(BDK_UNSUPPORTED, "warp_n must be a power of two (chunk swizzle)");
 
   bdk_cache* c = new bdk_cache();
   c->desc = *d;

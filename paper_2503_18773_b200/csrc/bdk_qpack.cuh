@@ -104,16 +104,20 @@ __device__ inline void qpass_token(const __half* src, int ld, int n_r, int d, in
         }
       }
     } else {
-      for (int i = 0; i < d / 32; ++i) {
+      // g < 32 (a power of two dividing d): lanes form aligned g-lane
+      // segments; lanes past d (d < 32 or d % 32 != 0) carry neutral values
+      for (int i = 0; i < (d + 31) / 32; ++i) {
         const int c = i * 32 + lane;
-        const float x = __half2float(row[c]);
-        float lo = x, hi = x;
-        int zfirst = x == 0.0f ? c : 0x7fffffff;
+        const bool valid = c < d;
+        const float x = valid ? __half2float(row[c]) : 0.0f;
+        float lo = valid ? x : INFINITY, hi = valid ? x : -INFINITY;
+        int zfirst = valid && x == 0.0f ? c : 0x7fffffff;
         for (int o = g / 2; o >= 1; o >>= 1) {
           lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
           hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
           zfirst = min(zfirst, __shfl_xor_sync(0xffffffffu, zfirst, o));
         }
+        if (!valid) continue;  // after the shuffles: every lane took part
         if (lo == 0.0f) lo = __half2float(row[zfirst]);
         if (hi == 0.0f) hi = __half2float(row[zfirst]);
         float s, z;

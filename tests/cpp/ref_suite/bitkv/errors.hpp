@@ -1,0 +1,3 @@
+// bitkv/errors.hpp -> the B200 drop-in (include/bitkv_b200.hpp)
+#pragma once
+#include "bitkv_b200.hpp"
