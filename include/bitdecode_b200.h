@@ -187,6 +187,40 @@ BDK_API bdk_status bdk_peer_merge(const float* const* parts, uint32_t* const* fl
                                   uint32_t world, uint32_t rank, uint64_t step, uint32_t rows,
                                   uint32_t d, float* out_dev, float* out_lse_dev, int* err_dev,
                                   uint64_t timeout_ns, void* stream);
+/* ------------------------------------------------ attention internals
+ * The reference's decode decomposition (attention.hpp:17-70), on the device,
+ * host buffers in and out, synchronous.  A PartialOutput state is three
+ * arrays: o [rows][d] (unnormalized), m [rows] (running max, -inf initially),
+ * l [rows] (running exp-sum, 0 initially).
+ * attend_tile (attention.cpp:52-90): one online-softmax step over tile_n
+ * tokens k/v [tile_n][d]; state in/out.  warp_n only picks the row-max
+ * partition, which does not change the result. */
+BDK_API bdk_status bdk_attend_tile_host(float* o, float* m, float* l, uint32_t rows, uint32_t d,
+                                        const float* q, const float* k, const float* v,
+                                        uint32_t tile_n, float scale, uint32_t warp_n,
+                                        int32_t device);
+/* partitioned_rowmax (attention.cpp:32-50): ShapeError unless warp_n | cols. */
+BDK_API bdk_status bdk_partitioned_rowmax_host(const float* s, uint32_t rows, uint32_t cols,
+                                               uint32_t warp_n, float* out, int32_t device);
+/* residual_attend (attention.cpp:92-105): one tile over the res_len residual
+ * tokens of cell (b, h); state in/out; StateError if the residual is empty.
+ * (The block build of a full residual is bdk_build_block.) */
+BDK_API bdk_status bdk_residual_attend_host(const bdk_cache* cache, uint32_t b, uint32_t h,
+                                            const float* q, uint32_t q_rows, float scale,
+                                            float* o, float* m, float* l);
+/* packed_attend (attention.cpp:107-140): the packed segment of cell (b, h)
+ * in tiles of tile_n, num_splits contiguous tile ranges; writes the
+ * *n_parts non-empty splits' states (capacity max(1, num_splits) each). */
+BDK_API bdk_status bdk_packed_attend_host(const bdk_cache* cache, uint32_t b, uint32_t h,
+                                          const float* q, uint32_t q_rows, uint32_t tile_n,
+                                          uint32_t num_splits, float scale, float* o, float* m,
+                                          float* l, uint32_t* n_parts);
+/* combine (attention.cpp:142-162) of n_parts states (o [n_parts][rows][d],
+ * m/l [n_parts][rows]) -> out [rows][d]; EmptyInput when n_parts == 0. */
+BDK_API bdk_status bdk_combine_host(const float* o, const float* m, const float* l,
+                                    uint32_t n_parts, uint32_t rows, uint32_t d, float* out,
+                                    int32_t device);
+
 /* 0 = fast (fp16 P), 1 = precise PV (P = P_hi + P_lo) */
 BDK_API bdk_status bdk_set_precise(bdk_cache* cache, int precise);
 

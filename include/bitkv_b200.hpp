@@ -16,6 +16,7 @@
 // the reference grows host vectors) and a CUDA device ordinal.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <bit>
 #include <cmath>
@@ -596,7 +597,7 @@ class KVCache {  // kvcache.hpp:103-189, cache resident in HBM
   }
   // KVCache::build_block (kvcache.cpp:208-219): pack the full residual on the
   // device without committing
-  PackedBlock build_block(size_t b, size_t h) {
+  PackedBlock build_block(size_t b, size_t h) const {
     PackedBlock blk = empty_block();
     detail::check(bdk_build_block(h_, static_cast<uint32_t>(b), static_cast<uint32_t>(h),
                                   blk.k_words.data(), blk.v_words.data(),
@@ -735,6 +736,134 @@ struct AttnOutput {  // attention.hpp:73-84
   float* row(size_t b, size_t h) { return data.data() + (b * heads + h) * d; }
   const float* row(size_t b, size_t h) const { return data.data() + (b * heads + h) * d; }
 };
+
+// The reference's decode decomposition (attention.hpp:17-70).  Every call
+// runs on the device (bdk_span.cu) through the C-ABI; the structs are the
+// reference's host-side value types.
+struct PartialOutput {  // attention.hpp:17-26
+  size_t rows = 0;
+  size_t d = 0;
+  std::vector<float> o;  // rows * d, unnormalized
+  std::vector<float> m;  // rows, starts at -inf
+  std::vector<float> l;  // rows, starts at 0
+  static PartialOutput init(size_t rows, size_t d) {
+    PartialOutput p;
+    p.rows = rows;
+    p.d = d;
+    p.o.assign(rows * d, 0.0f);
+    p.m.assign(rows, -INFINITY);
+    p.l.assign(rows, 0.0f);
+    return p;
+  }
+};
+
+// attention.hpp:28-36.  The device kernels keep their own staging in shared
+// memory; the struct stays for signature compatibility.
+struct StagingBuffer {
+  std::vector<float> partition_max;
+  std::vector<float> p_tile;
+  void reserve(size_t warp_n, size_t tile_m, size_t tile_n) {
+    partition_max.resize(warp_n);
+    p_tile.resize(tile_m * tile_n);
+  }
+};
+
+namespace detail {
+// device of the cache-less calls (attend_tile, partitioned_rowmax, combine)
+inline int& compute_device() {
+  static int dev = 0;
+  return dev;
+}
+}  // namespace detail
+
+// partitioned_rowmax (attention.cpp:32-50)
+inline void partitioned_rowmax(const float* s, size_t rows, size_t cols, size_t warp_n,
+                               StagingBuffer& buf, float* rowmax_out) {
+  if (warp_n != 0) buf.partition_max.resize(warp_n);
+  detail::check(bdk_partitioned_rowmax_host(s, static_cast<uint32_t>(rows),
+                                            static_cast<uint32_t>(cols),
+                                            static_cast<uint32_t>(warp_n), rowmax_out,
+                                            detail::compute_device()));
+}
+
+// attend_tile (attention.cpp:52-90): one online-softmax step
+inline void attend_tile(PartialOutput& state, const float* q, const float* k, const float* v,
+                        size_t tile_n, size_t d, float scale_factor, size_t warp_n,
+                        StagingBuffer& buf) {
+  (void)buf;
+  if (state.d != d || state.o.size() != state.rows * d)
+    throw ShapeError("attend_tile: state shape does not match d");
+  detail::check(bdk_attend_tile_host(state.o.data(), state.m.data(), state.l.data(),
+                                     static_cast<uint32_t>(state.rows), static_cast<uint32_t>(d),
+                                     q, k, v, static_cast<uint32_t>(tile_n), scale_factor,
+                                     static_cast<uint32_t>(warp_n), detail::compute_device()));
+}
+
+// residual_attend (attention.cpp:92-105): attention over the residual of
+// cell (b, h); the packed block of a full residual, for the caller to commit
+inline std::optional<PackedBlock> residual_attend(const KVCache& cache, size_t b, size_t h,
+                                                  const float* q, size_t q_rows,
+                                                  float scale_factor, size_t warp_n,
+                                                  PartialOutput& state, StagingBuffer& buf) {
+  (void)warp_n;
+  (void)buf;
+  if (cache.res_len(b, h) == 0) throw StateError("residual_attend: residual cache is empty");
+  if (state.rows != q_rows) throw ShapeError("residual_attend: state rows != q rows");
+  if (state.d != cache.head_dim()) throw ShapeError("residual_attend: state d != head_dim");
+  detail::check(bdk_residual_attend_host(cache.handle(), static_cast<uint32_t>(b),
+                                         static_cast<uint32_t>(h), q,
+                                         static_cast<uint32_t>(q_rows), scale_factor,
+                                         state.o.data(), state.m.data(), state.l.data()));
+  if (cache.res_len(b, h) == cache.n_r()) return cache.build_block(b, h);
+  return std::nullopt;
+}
+
+// packed_attend (attention.cpp:107-140): one state per non-empty split
+inline std::vector<PartialOutput> packed_attend(const KVCache& cache, size_t b, size_t h,
+                                                const float* q, size_t q_rows, size_t tile_n,
+                                                size_t num_splits, float scale_factor,
+                                                size_t warp_n) {
+  (void)warp_n;
+  const size_t d = cache.head_dim();
+  const size_t cap = std::max<size_t>(1, num_splits);
+  std::vector<float> o(cap * q_rows * d), m(cap * q_rows), l(cap * q_rows);
+  uint32_t n = 0;
+  detail::check(bdk_packed_attend_host(cache.handle(), static_cast<uint32_t>(b),
+                                       static_cast<uint32_t>(h), q,
+                                       static_cast<uint32_t>(q_rows),
+                                       static_cast<uint32_t>(tile_n),
+                                       static_cast<uint32_t>(num_splits), scale_factor, o.data(),
+                                       m.data(), l.data(), &n));
+  std::vector<PartialOutput> parts(n);
+  for (uint32_t p = 0; p < n; ++p) {
+    parts[p].rows = q_rows;
+    parts[p].d = d;
+    parts[p].o.assign(o.begin() + p * q_rows * d, o.begin() + (p + 1) * q_rows * d);
+    parts[p].m.assign(m.begin() + p * q_rows, m.begin() + (p + 1) * q_rows);
+    parts[p].l.assign(l.begin() + p * q_rows, l.begin() + (p + 1) * q_rows);
+  }
+  return parts;
+}
+
+// combine (attention.cpp:142-162): LSE reduction of the partial states
+inline std::vector<float> combine(std::span<const PartialOutput> partials) {
+  if (partials.empty()) throw EmptyInput("combine: no partial outputs");
+  const size_t rows = partials[0].rows, d = partials[0].d;
+  for (const auto& p : partials)
+    if (p.rows != rows || p.d != d) throw ShapeError("combine: partial shapes differ");
+  std::vector<float> o, m, l, out(rows * d);
+  o.reserve(partials.size() * rows * d);
+  for (const auto& p : partials) {
+    o.insert(o.end(), p.o.begin(), p.o.end());
+    m.insert(m.end(), p.m.begin(), p.m.end());
+    l.insert(l.end(), p.l.begin(), p.l.end());
+  }
+  detail::check(bdk_combine_host(o.data(), m.data(), l.data(),
+                                 static_cast<uint32_t>(partials.size()),
+                                 static_cast<uint32_t>(rows), static_cast<uint32_t>(d), out.data(),
+                                 detail::compute_device()));
+  return out;
+}
 
 // decode_step (attention.hpp:87-88, attention.cpp:164-242)
 inline AttnOutput decode_step(KVCache& cache, const AttentionConfig& cfg, const Tensor& q,

@@ -68,6 +68,13 @@ SIGNATURES = {
     "bdk_decode_partial": (C.c_int, [vp, C.POINTER(AttnConfig), vp, vp, vp, u32, u32, u32, vp,
                                      vp, vp]),
     "bdk_merge_partials": (C.c_int, [vp, vp, u32, u32, u32, C.c_uint64, C.c_uint64, vp, vp]),
+    "bdk_attend_tile_host": (C.c_int, [vp, vp, vp, u32, u32, vp, vp, vp, u32, C.c_float, u32,
+                                       i32]),
+    "bdk_partitioned_rowmax_host": (C.c_int, [vp, u32, u32, u32, vp, i32]),
+    "bdk_residual_attend_host": (C.c_int, [vp, u32, u32, vp, u32, C.c_float, vp, vp, vp]),
+    "bdk_packed_attend_host": (C.c_int, [vp, u32, u32, vp, u32, u32, u32, C.c_float, vp, vp, vp,
+                                         C.POINTER(u32)]),
+    "bdk_combine_host": (C.c_int, [vp, vp, vp, u32, u32, u32, vp, i32]),
     "bdk_set_precise": (C.c_int, [vp, C.c_int]),
     "bdk_read_block": (C.c_int, [vp, u32, u32, u32, u16p, u16p, u16p, u16p]),
     "bdk_adopt_block": (C.c_int, [vp, u32, u32, u16p, u16p, u16p, u16p]),

@@ -778,6 +778,107 @@ def decode_partial(cache: KVCache, cfg: AttentionConfig, q, k_new=None, v_new=No
     return o, lse
 
 
+# ------------------------------------------------- attention internals
+# The reference's decode decomposition (attention.hpp:17-70), on the device
+# (bdk_span.cu); numpy fp32 in and out, synchronous.
+
+@dataclass
+class PartialOutput:
+    """PartialOutput (attention.hpp:17-26): unnormalized o [rows, d], running
+    max m [rows] (-inf initially) and exp-sum l [rows] (0 initially)."""
+    o: np.ndarray
+    m: np.ndarray
+    l: np.ndarray
+
+    @property
+    def rows(self) -> int:
+        return self.o.shape[0]
+
+    @property
+    def d(self) -> int:
+        return self.o.shape[1]
+
+    @staticmethod
+    def init(rows: int, d: int) -> "PartialOutput":
+        return PartialOutput(np.zeros((rows, d), np.float32), np.full(rows, -np.inf, np.float32),
+                             np.zeros(rows, np.float32))
+
+
+def _f32(x) -> np.ndarray:
+    return np.ascontiguousarray(x, np.float32)
+
+
+def partitioned_rowmax(s, warp_n: int, device: int = 0) -> np.ndarray:
+    """partitioned_rowmax (attention.cpp:32-50) of s [rows, cols]."""
+    x = _f32(s)
+    rows, cols = x.shape
+    out = np.zeros(rows, np.float32)
+    _check(_L.load().bdk_partitioned_rowmax_host(x.ctypes.data, rows, cols, warp_n,
+                                                 out.ctypes.data, device))
+    return out
+
+
+def attend_tile(state: PartialOutput, q, k, v, scale: float, warp_n: int = 1,
+                device: int = 0) -> None:
+    """attend_tile (attention.cpp:52-90): one online-softmax step over the
+    tokens of k/v [tile_n, d]; updates state in place."""
+    q, k, v = _f32(q), _f32(k), _f32(v)
+    if k.shape != v.shape or k.shape[1] != state.d or q.shape != (state.rows, state.d):
+        raise ShapeError("attend_tile: q [rows, d], k/v [tile_n, d] must match the state")
+    _check(_L.load().bdk_attend_tile_host(state.o.ctypes.data, state.m.ctypes.data,
+                                          state.l.ctypes.data, state.rows, state.d,
+                                          q.ctypes.data, k.ctypes.data, v.ctypes.data,
+                                          k.shape[0], scale, warp_n, device))
+
+
+def residual_attend(cache: "KVCache", b: int, h: int, q, scale: float,
+                    state: PartialOutput, warp_n: int = 1):
+    """residual_attend (attention.cpp:92-105): attention over the residual of
+    cell (b, h) into state; returns the PackedBlock of a full residual (for
+    the caller to commit) or None."""
+    q = _f32(q)
+    if q.shape != (state.rows, state.d):
+        raise ShapeError("residual_attend: state rows != q rows")
+    _check(_L.load().bdk_residual_attend_host(cache.handle(), b, h, q.ctypes.data, q.shape[0],
+                                              scale, state.o.ctypes.data, state.m.ctypes.data,
+                                              state.l.ctypes.data))
+    return cache.build_block(b, h) if cache.res_len(b, h) == cache.n_r() else None
+
+
+def packed_attend(cache: "KVCache", b: int, h: int, q, tile_n: int, num_splits: int,
+                  scale: float, warp_n: int = 1) -> list:
+    """packed_attend (attention.cpp:107-140): one PartialOutput per non-empty
+    split of the packed segment of cell (b, h)."""
+    q = _f32(q)
+    rows, d = q.shape
+    cap = max(1, num_splits)
+    o = np.zeros((cap, rows, d), np.float32)
+    m = np.zeros((cap, rows), np.float32)
+    l = np.zeros((cap, rows), np.float32)
+    n = C.c_uint32(0)
+    _check(_L.load().bdk_packed_attend_host(cache.handle(), b, h, q.ctypes.data, rows, tile_n,
+                                            num_splits, scale, o.ctypes.data, m.ctypes.data,
+                                            l.ctypes.data, C.byref(n)))
+    return [PartialOutput(o[i].copy(), m[i].copy(), l[i].copy()) for i in range(n.value)]
+
+
+def combine(partials, device: int = 0) -> np.ndarray:
+    """combine (attention.cpp:142-162): O = sum o_i w_i / sum l_i w_i with
+    w_i = e^(m_i - max m) -> [rows, d]."""
+    if len(partials) == 0:
+        raise EmptyInput("combine: no partial outputs")
+    rows, d = partials[0].o.shape
+    if any(p.o.shape != (rows, d) for p in partials):
+        raise ShapeError("combine: partial shapes differ")
+    o = _f32(np.stack([p.o for p in partials]))
+    m = _f32(np.stack([p.m for p in partials]))
+    l = _f32(np.stack([p.l for p in partials]))
+    out = np.zeros((rows, d), np.float32)
+    _check(_L.load().bdk_combine_host(o.ctypes.data, m.ctypes.data, l.ctypes.data, len(partials),
+                                      rows, d, out.ctypes.data, device))
+    return out
+
+
 def merge_partials(o_parts, lse_parts, out=None):
     """combine (attention.cpp:142-162) of normalized partials:
     o_parts [n, rows..., d], lse_parts [n, rows...] (CUDA fp32; the part

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libbitdecode_b200.so")
-SOURCES = ["bdk_kernels.cu", "bdk_decode_fast.cu", "bdk_api.cu"]
+SOURCES = ["bdk_kernels.cu", "bdk_decode_fast.cu", "bdk_span.cu", "bdk_api.cu"]
 HEADERS = ["bdk_common.cuh", "bdk_frag.cuh", "bdk_qpack.cuh", "bdk_qpack_fast.cuh", "bdk_launch.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -37,6 +37,9 @@ struct bdk_cache {
   float* part_o = nullptr;
   float* part_ml = nullptr;
   size_t part_floats = 0, part_ml_floats = 0;
+  // span-path partial states (bdk_span.cu)
+  float* span_parts = nullptr;
+  size_t span_floats = 0;
   // host-API staging (pinned host + device)
   void* h_stage = nullptr;
   void* d_stage = nullptr;
@@ -151,6 +154,14 @@ bdk_status validate(const bdk_attn_config* cfg) {
   return BDK_OK;
 }
 
+// geometry the tensor-core decode kernels serve; anything else the reference
+// accepts runs on the span path (bdk_span.cu)
+bool exact_ok(const bdk_cache* c, const bdk_attn_config* cfg) {
+  return bdk::fast_path_ok(c->dev.G) && cfg->heads_q / cfg->heads_kv <= 8;
+}
+
+constexpr size_t kSpanSmemMax = 227u << 10;
+
 // decode_step shape checks (attention.cpp:164-179) + capacity of the append
 bdk_status check_decode(bdk_cache* c, const bdk_attn_config* cfg, bool appends) {
   if (!c || !cfg) return fail(BDK_INVALID_ARGUMENT, "null argument");
@@ -159,12 +170,11 @@ bdk_status check_decode(bdk_cache* c, const bdk_attn_config* cfg, bool appends) 
   if (cfg->batch != c->desc.batch || cfg->heads_kv != c->desc.heads_kv ||
       cfg->head_dim != c->desc.head_dim)
     return fail(BDK_SHAPE_ERROR, "decode_step: cache geometry does not match config");
-  if (cfg->heads_q / cfg->heads_kv > 8)
-    return fail(BDK_UNSUPPORTED, "n_group > 8 is outside the decode kernel envelope");
-  if (!bdk::fast_path_ok(c->dev.G))
-    return fail(BDK_UNSUPPORTED,
-                "geometry outside the sm_100a decode kernels' envelope (head_dim 128, warp_n in "
-                "{1,2,4,8}, group_size % 16 == 0, channel-wise group_size % (8*16/bits) == 0)");
+  if (!exact_ok(c, cfg)) {
+    const int tile = static_cast<int>(std::max<uint32_t>(cfg->tile_n, c->dev.G.n_r));
+    if (bdk::span_smem_bytes(cfg->heads_q / cfg->heads_kv, cfg->head_dim, tile) > kSpanSmemMax)
+      return fail(BDK_UNSUPPORTED, "n_group * (head_dim + max(tile_n, N_r)) exceeds shared memory");
+  }
   if (appends) {
     const int n_r = c->dev.G.n_r;
     for (size_t i = 0; i < c->res_len.size(); ++i) {
@@ -318,10 +328,75 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
   return BDK_OK;
 }
 
+bdk_status ensure_span(bdk_cache* c, size_t floats) {
+  if (floats <= c->span_floats) return BDK_OK;
+  if (c->span_parts) cudaFree(c->span_parts);
+  c->span_parts = nullptr;
+  BDK_CUDA(cudaMalloc(&c->span_parts, floats * sizeof(float)), "cudaMalloc(span parts)");
+  c->span_floats = floats;
+  return BDK_OK;
+}
+
+// decode_step on the span path (bdk_span.cu): the reference's own
+// decomposition -- residual window (with the appended token) as part 0, then
+// cfg->num_splits packed splits of cfg->tile_n tiles -- combined in that
+// order, then the flush of any residual the step filled
+bdk_status run_decode_span(bdk_cache* c, const bdk_attn_config* cfg, const void* q,
+                           const void* k_new, const void* v_new, float* out, float* lse,
+                           int blk_begin, int blk_end, cudaStream_t stream, bool no_res) {
+  const int cells = static_cast<int>(c->desc.batch * c->desc.heads_kv);
+  const int ng = static_cast<int>(cfg->heads_q / cfg->heads_kv), d = c->desc.head_dim;
+  bdk::SpanArgs a;
+  a.c = c->dev;
+  a.q16 = static_cast<const __half*>(q);
+  a.q_scale = 1.0f / std::sqrt(static_cast<float>(d));  // attention.cpp:198
+  a.k_new = static_cast<const __half*>(k_new);
+  a.v_new = static_cast<const __half*>(v_new);
+  a.heads_q = static_cast<int>(cfg->heads_q);
+  a.rows = ng;
+  a.d = d;
+  a.residual = no_res ? 0 : 1;
+  a.tile_n = static_cast<int>(cfg->tile_n);
+  a.splits = static_cast<int>(cfg->num_splits);
+  a.blk_begin = std::max(0, blk_begin);
+  a.blk_end = blk_end;
+  a.warp_n = static_cast<int>(cfg->warp_n);
+  a.n_parts = a.residual + a.splits;
+  bdk_status s = ensure_span(c, (size_t)cells * a.n_parts * ng * (d + 2));
+  if (s) return s;
+  a.parts = c->span_parts;
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  BDK_CUDA(bdk::launch_span_parts(a, cells, stream), "span launch");
+  BDK_CUDA(bdk::launch_span_combine(c->span_parts, cells, a.n_parts, ng, d,
+                                    static_cast<int>(c->desc.heads_kv),
+                                    static_cast<int>(cfg->heads_q), out, lse,
+                                    k_new != nullptr ? c->dev.res_len : nullptr, stream),
+           "span combine launch");
+  c->launches += 2;
+  if (k_new != nullptr) {
+    bool full = false;
+    for (int i = 0; i < cells; ++i) full |= c->res_len[i] + 1 == c->dev.G.n_r;
+    if (full) {
+      BDK_CUDA(bdk::launch_flush_full(c->dev, stream), "flush launch");
+      c->launches += 1;
+      c->blocks_written = true;
+    }
+    for (int i = 0; i < cells; ++i) {
+      if (++c->res_len[i] == c->dev.G.n_r) {
+        c->res_len[i] = 0;
+        c->packed_blocks[i] += 1;
+      }
+    }
+  }
+  return BDK_OK;
+}
+
 bdk_status run_decode(bdk_cache* c, const bdk_attn_config* cfg, const void* q, const void* k_new,
                       const void* v_new, float* out, float* lse, int blk_begin, int blk_end,
                       cudaStream_t stream, bool no_res = false) {
   const int cells = static_cast<int>(c->desc.batch * c->desc.heads_kv);
+  if (!exact_ok(c, cfg))
+    return run_decode_span(c, cfg, q, k_new, v_new, out, lse, blk_begin, blk_end, stream, no_res);
   if (!c->precise && bdk::fast_decode_ok(c->dev.G, static_cast<int>(cfg->heads_q / cfg->heads_kv)))
     return run_decode_fast(c, cfg, q, k_new, v_new, out, lse, std::max(0, blk_begin), blk_end,
                            stream, no_res);
@@ -487,6 +562,7 @@ bdk_status bdk_cache_destroy(bdk_cache* c) {
   cudaFree(c->dev.res_len);
   cudaFree(c->part_o);
   cudaFree(c->part_ml);
+  cudaFree(c->span_parts);
   cudaFree(c->unit_off);
   cudaFree(c->counters);
   cudaFree(c->slots);
@@ -652,6 +728,196 @@ bdk_status bdk_merge_partials(const float* o, const float* lse, uint32_t n_parts
                                       static_cast<int>(d), o_stride, lse_stride, out,
                                       as_stream(stream)),
            "merge launch");
+  return BDK_OK;
+}
+
+// ------------------------------------------------- attention internals
+// attend_tile / partitioned_rowmax / residual_attend / packed_attend /
+// combine (attention.hpp:17-70) on the device (bdk_span.cu): host buffers in
+// and out, synchronous.  Same validation and error classes as the reference.
+namespace {
+struct DevF {  // scoped device float buffer
+  float* p = nullptr;
+  ~DevF() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t n) { return cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(float)); }
+};
+
+bdk_status span_fits(uint32_t rows, uint32_t d, uint32_t tile) {
+  if (bdk::span_smem_bytes(rows, d, tile) > kSpanSmemMax)
+    return fail(BDK_UNSUPPORTED, "rows * (d + tile) exceeds shared memory");
+  return BDK_OK;
+}
+
+// state [rows*d o | rows m | rows l] <-> the three host arrays
+bdk_status put_state(float* dst, const float* o, const float* m, const float* l, size_t rows,
+                     size_t d) {
+  BDK_CUDA(cudaMemcpy(dst, o, rows * d * 4, cudaMemcpyHostToDevice), "H2D state");
+  BDK_CUDA(cudaMemcpy(dst + rows * d, m, rows * 4, cudaMemcpyHostToDevice), "H2D state");
+  BDK_CUDA(cudaMemcpy(dst + rows * d + rows, l, rows * 4, cudaMemcpyHostToDevice), "H2D state");
+  return BDK_OK;
+}
+bdk_status get_state(const float* src, float* o, float* m, float* l, size_t rows, size_t d) {
+  BDK_CUDA(cudaMemcpy(o, src, rows * d * 4, cudaMemcpyDeviceToHost), "D2H state");
+  BDK_CUDA(cudaMemcpy(m, src + rows * d, rows * 4, cudaMemcpyDeviceToHost), "D2H state");
+  BDK_CUDA(cudaMemcpy(l, src + rows * d + rows, rows * 4, cudaMemcpyDeviceToHost), "D2H state");
+  return BDK_OK;
+}
+}  // namespace
+
+bdk_status bdk_attend_tile_host(float* o, float* m, float* l, uint32_t rows, uint32_t d,
+                                const float* q, const float* k, const float* v, uint32_t tile_n,
+                                float scale, uint32_t warp_n, int32_t device) {
+  if (!o || !m || !l || !q || (tile_n && (!k || !v)))
+    return fail(BDK_INVALID_ARGUMENT, "null argument");
+  if (rows == 0 || d == 0 || tile_n == 0) return BDK_OK;
+  bdk_status s = span_fits(rows, d, tile_n);
+  if (s) return s;
+  BDK_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  DevF bq, bk, bv, bs;
+  BDK_CUDA(bq.alloc((size_t)rows * d), "cudaMalloc");
+  BDK_CUDA(bk.alloc((size_t)tile_n * d), "cudaMalloc");
+  BDK_CUDA(bv.alloc((size_t)tile_n * d), "cudaMalloc");
+  BDK_CUDA(bs.alloc((size_t)rows * (d + 2)), "cudaMalloc");
+  BDK_CUDA(cudaMemcpy(bq.p, q, (size_t)rows * d * 4, cudaMemcpyHostToDevice), "H2D");
+  BDK_CUDA(cudaMemcpy(bk.p, k, (size_t)tile_n * d * 4, cudaMemcpyHostToDevice), "H2D");
+  BDK_CUDA(cudaMemcpy(bv.p, v, (size_t)tile_n * d * 4, cudaMemcpyHostToDevice), "H2D");
+  if ((s = put_state(bs.p, o, m, l, rows, d))) return s;
+  bdk::SpanArgs a;
+  a.source = bdk::kSpanFp32;
+  a.k32 = bk.p;
+  a.v32 = bv.p;
+  a.len32 = static_cast<int>(tile_n);
+  a.q32 = bq.p;
+  a.scale = scale;
+  a.rows = static_cast<int>(rows);
+  a.d = static_cast<int>(d);
+  a.residual = 0;
+  a.tile_n = static_cast<int>(tile_n);
+  a.warp_n = static_cast<int>(warp_n);
+  a.keep_state = 1;
+  a.parts = bs.p;
+  a.n_parts = 1;
+  BDK_CUDA(bdk::launch_span_parts(a, 1, nullptr), "attend_tile launch");
+  return get_state(bs.p, o, m, l, rows, d);
+}
+
+bdk_status bdk_partitioned_rowmax_host(const float* sc, uint32_t rows, uint32_t cols,
+                                       uint32_t warp_n, float* out, int32_t device) {
+  if (warp_n == 0 || cols % warp_n != 0)
+    return fail(BDK_SHAPE_ERROR,
+                "partitioned_rowmax: cols must divide evenly across warp_n partitions");
+  if (!sc || !out) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  if (rows == 0) return BDK_OK;
+  BDK_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  DevF bs, bo;
+  BDK_CUDA(bs.alloc((size_t)rows * cols), "cudaMalloc");
+  BDK_CUDA(bo.alloc(rows), "cudaMalloc");
+  BDK_CUDA(cudaMemcpy(bs.p, sc, (size_t)rows * cols * 4, cudaMemcpyHostToDevice), "H2D");
+  BDK_CUDA(bdk::launch_partitioned_rowmax(bs.p, (int)rows, (int)cols, (int)warp_n, bo.p, nullptr),
+           "rowmax launch");
+  BDK_CUDA(cudaMemcpy(out, bo.p, rows * 4, cudaMemcpyDeviceToHost), "D2H");
+  return BDK_OK;
+}
+
+bdk_status bdk_residual_attend_host(const bdk_cache* c, uint32_t b, uint32_t h, const float* q,
+                                    uint32_t q_rows, float scale, float* o, float* m, float* l) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  if (!q || !o || !m || !l) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  const int i = cell_of(c, b, h);
+  if (c->res_len[i] == 0) return fail(BDK_STATE_ERROR, "residual_attend: residual cache is empty");
+  if (q_rows == 0) return BDK_OK;
+  const uint32_t d = c->desc.head_dim;
+  if ((s = span_fits(q_rows, d, c->dev.G.n_r))) return s;
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevF bq, bs;
+  BDK_CUDA(bq.alloc((size_t)q_rows * d), "cudaMalloc");
+  BDK_CUDA(bs.alloc((size_t)q_rows * (d + 2)), "cudaMalloc");
+  BDK_CUDA(cudaMemcpy(bq.p, q, (size_t)q_rows * d * 4, cudaMemcpyHostToDevice), "H2D");
+  if ((s = put_state(bs.p, o, m, l, q_rows, d))) return s;
+  bdk::SpanArgs a;
+  a.c = c->dev;
+  a.q32 = bq.p;
+  a.scale = scale;
+  a.rows = static_cast<int>(q_rows);
+  a.d = static_cast<int>(d);
+  a.cell0 = i;
+  a.residual = 1;
+  a.splits = 0;
+  a.tile_n = c->dev.G.n_r;
+  a.keep_state = 1;
+  a.parts = bs.p;
+  a.n_parts = 1;
+  c->launches += 1;
+  BDK_CUDA(bdk::launch_span_parts(a, 1, nullptr), "residual_attend launch");
+  return get_state(bs.p, o, m, l, q_rows, d);
+}
+
+bdk_status bdk_packed_attend_host(const bdk_cache* c, uint32_t b, uint32_t h, const float* q,
+                                  uint32_t q_rows, uint32_t tile_n, uint32_t num_splits,
+                                  float scale, float* o, float* m, float* l, uint32_t* n_parts) {
+  bdk_status s = check_cell(c, b, h);
+  if (s) return s;
+  if (!q || !o || !m || !l || !n_parts) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  if (tile_n == 0) return fail(BDK_SHAPE_ERROR, "packed_attend: tile_n must be > 0");
+  *n_parts = 0;
+  const int i = cell_of(c, b, h);
+  const uint64_t plen = (uint64_t)c->packed_blocks[i] * c->dev.G.n_r;
+  if (plen == 0 || q_rows == 0) return BDK_OK;
+  const uint32_t d = c->desc.head_dim;
+  if ((s = span_fits(q_rows, d, std::max<uint32_t>(tile_n, c->dev.G.n_r)))) return s;
+  // splits past the tile count are empty (attention.cpp:124-130) and omitted
+  const uint64_t n_tiles = (plen + tile_n - 1) / tile_n;
+  const uint32_t splits = (uint32_t)std::min<uint64_t>(std::max<uint32_t>(1, num_splits), n_tiles);
+  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevF bq, bs;
+  const size_t stride = (size_t)q_rows * (d + 2);
+  BDK_CUDA(bq.alloc((size_t)q_rows * d), "cudaMalloc");
+  BDK_CUDA(bs.alloc(stride * splits), "cudaMalloc");
+  BDK_CUDA(cudaMemcpy(bq.p, q, (size_t)q_rows * d * 4, cudaMemcpyHostToDevice), "H2D");
+  bdk::SpanArgs a;
+  a.c = c->dev;
+  a.q32 = bq.p;
+  a.scale = scale;
+  a.rows = static_cast<int>(q_rows);
+  a.d = static_cast<int>(d);
+  a.cell0 = i;
+  a.residual = 0;
+  a.tile_n = static_cast<int>(tile_n);
+  a.splits = static_cast<int>(splits);
+  a.parts = bs.p;
+  a.n_parts = static_cast<int>(splits);
+  c->launches += 1;
+  BDK_CUDA(bdk::launch_span_parts(a, 1, nullptr), "packed_attend launch");
+  for (uint32_t p = 0; p < splits; ++p)
+    if ((s = get_state(bs.p + p * stride, o + (size_t)p * q_rows * d, m + (size_t)p * q_rows,
+                       l + (size_t)p * q_rows, q_rows, d)))
+      return s;
+  *n_parts = splits;
+  return BDK_OK;
+}
+
+bdk_status bdk_combine_host(const float* o, const float* m, const float* l, uint32_t n_parts,
+                            uint32_t rows, uint32_t d, float* out, int32_t device) {
+  if (n_parts == 0) return fail(BDK_EMPTY_INPUT, "combine: no partial outputs");
+  if (!o || !m || !l || !out) return fail(BDK_INVALID_ARGUMENT, "null argument");
+  if (rows == 0 || d == 0) return BDK_OK;
+  BDK_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  const size_t stride = (size_t)rows * (d + 2);
+  DevF bs, bo;
+  BDK_CUDA(bs.alloc(stride * n_parts), "cudaMalloc");
+  BDK_CUDA(bo.alloc((size_t)rows * d), "cudaMalloc");
+  for (uint32_t p = 0; p < n_parts; ++p) {
+    bdk_status s = put_state(bs.p + p * stride, o + (size_t)p * rows * d, m + (size_t)p * rows,
+                             l + (size_t)p * rows, rows, d);
+    if (s) return s;
+  }
+  BDK_CUDA(bdk::launch_span_combine(bs.p, 1, (int)n_parts, (int)rows, (int)d, 1, (int)rows, bo.p,
+                                    nullptr, nullptr, nullptr),
+           "combine launch");
+  BDK_CUDA(cudaMemcpy(out, bo.p, (size_t)rows * d * 4, cudaMemcpyDeviceToHost), "D2H");
   return BDK_OK;
 }
 

@@ -211,4 +211,30 @@ __device__ __forceinline__ float warp_max_xor(float v, int from) {
   return v;
 }
 
+// ------------------------------------------------------ element readback
+// Element (token t, channel ch) of one block record, dequantized exactly as
+// packed_tile stages it (kvcache.cpp:289-309): round_f16(code*scale + zero)
+// in fp32 (the fp32 product is exact); passthrough blocks hold raw fp16 bits.
+// which = 0 keys, 1 values.
+__device__ __forceinline__ __half packed_elem(const Geom& G, const uint8_t* rec, int t, int ch,
+                                              int which) {
+  const int rb = 16 * G.warp_n, P = G.pack;
+  const uint32_t mask = G.bits == 16 ? 0xFFFFu : ((1u << G.bits) - 1u);
+  const int wi = t / P, j = wi / 8;
+  const int p = field_of_token(t % P, P, G.interleave);
+  const uint8_t* words = rec + which * G.wbytes;
+  const uint16_t w = *reinterpret_cast<const uint16_t*>(
+      words + (size_t)ch * rb + ((j ^ swz(ch, G.warp_n)) << 4) + (wi % 8) * 2);
+  const uint32_t code = (w >> (p * G.bits)) & mask;
+  if (G.bits == 16) return __ushort_as_half(static_cast<uint16_t>(code));
+  const uint32_t* par =
+      reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes + (which ? G.kp_bytes : 0));
+  const int gi = (which == 0 && G.k_axis == 0) ? (t / G.g) * G.d + ch
+                                               : t * (G.d / G.g) + ch / G.g;
+  const uint32_t pr = par[gi];
+  const float s = __half2float(__ushort_as_half(static_cast<uint16_t>(pr & 0xFFFF)));
+  const float z = __half2float(__ushort_as_half(static_cast<uint16_t>(pr >> 16)));
+  return __float2half_rn(__fadd_rn(__fmul_rn(static_cast<float>(code), s), z));
+}
+
 }  // namespace bdk

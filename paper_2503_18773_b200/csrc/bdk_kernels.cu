@@ -117,43 +117,16 @@ __global__ void __launch_bounds__(256) flush_full_kernel(DevCache c) {
   }
 }
 
-// packed_tile dequant (kvcache.cpp:289-309): round_f16(code*scale + zero) in
-// fp32 exactly as the reference stages it (fp32 product is exact).
+// packed_tile dequant: blocks [blk0, blk0 + gridDim.x) of a cell -> fp16 rows
 __global__ void dequant_kernel(DevCache c, int cell, int blk0, __half* k_out, __half* v_out) {
   const Geom& G = c.G;
   const int blk = blk0 + blockIdx.x;
   const uint8_t* rec = c.records + ((size_t)cell * G.max_blocks + blk) * G.rec_bytes;
-  const int rb = 16 * G.warp_n, P = G.pack;
-  const uint32_t mask = G.bits == 16 ? 0xFFFFu : ((1u << G.bits) - 1u);
   for (int i = threadIdx.x; i < G.n_r * G.d; i += blockDim.x) {
     const int t = i / G.d, ch = i % G.d;
-    const int wi = t / P, j = wi / 8;
-    int p = 0;
-    for (; p < P; ++p)
-      if (wi * P + pos_token(p, P, G.interleave) == t) break;
-    for (int which = 0; which < 2; ++which) {
-      const uint8_t* words = rec + which * G.wbytes;
-      const uint16_t w = *reinterpret_cast<const uint16_t*>(
-          words + (size_t)ch * rb + ((j ^ swz(ch, G.warp_n)) << 4) + (wi % 8) * 2);
-      const uint32_t code = (w >> (p * G.bits)) & mask;
-      __half out;
-      if (G.bits == 16) {
-        out = __ushort_as_half(static_cast<uint16_t>(code));
-      } else {
-        const uint32_t* par =
-            reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes + (which ? G.kp_bytes : 0));
-        int gi;
-        if (which == 0 && G.k_axis == 0)
-          gi = (t / G.g) * G.d + ch;
-        else
-          gi = t * (G.d / G.g) + ch / G.g;
-        const uint32_t pr = par[gi];
-        const float s = __half2float(__ushort_as_half(static_cast<uint16_t>(pr & 0xFFFF)));
-        const float z = __half2float(__ushort_as_half(static_cast<uint16_t>(pr >> 16)));
-        out = __float2half_rn(__fadd_rn(__fmul_rn(static_cast<float>(code), s), z));
-      }
-      (which ? v_out : k_out)[(size_t)blockIdx.x * G.n_r * G.d + i] = out;
-    }
+    const size_t o = (size_t)blockIdx.x * G.n_r * G.d + i;
+    k_out[o] = packed_elem(G, rec, t, ch, 0);
+    v_out[o] = packed_elem(G, rec, t, ch, 1);
   }
 }
 

@@ -110,6 +110,45 @@ struct PeerMergeArgs {
 };
 cudaError_t launch_peer_merge(const PeerMergeArgs& a, cudaStream_t s);
 
+// General span attention (bdk_span.cu): decode_step for geometry outside the
+// fast kernels' envelope and the reference's attention internals
+// (attend_tile / residual_attend / packed_attend / combine).  One CTA per
+// (part, cell); a part is a cell's residual window or one split of its packed
+// segment, split by the reference's rule (attention.cpp:116-130).  A part's
+// state is [rows*d o | rows m | rows l] fp32, unnormalized (PartialOutput).
+enum SpanSource { kSpanCache = 0, kSpanFp32 = 1 };
+struct SpanArgs {
+  DevCache c;
+  int source = kSpanCache;
+  const float* k32 = nullptr;  // kSpanFp32: tokens [len32][d]
+  const float* v32 = nullptr;
+  int len32 = 0;
+  const __half* q16 = nullptr;  // [batch][heads_q][d], times q_scale in fp32 (decode)
+  const float* q32 = nullptr;   // [rows][d] as given (one cell)
+  float q_scale = 1.f, scale = 1.f;
+  const __half* k_new = nullptr;  // decode append rows [cells][d]; written by the residual part
+  const __half* v_new = nullptr;
+  int heads_q = 0, rows = 0, d = 0;
+  int cell0 = 0;
+  int residual = 1;  // part 0 of every cell is its residual window
+  int tile_n = 64, splits = 1;
+  int blk_begin = 0, blk_end = 1 << 30;
+  int warp_n = 1;
+  int keep_state = 0;  // parts already hold the initial state
+  float* parts = nullptr;  // [cells][n_parts][rows * (d + 2)]
+  int n_parts = 1;
+};
+// dynamic shared memory of one span CTA (tile = the longest tile it walks)
+size_t span_smem_bytes(int rows, int d, int tile);
+cudaError_t launch_span_parts(const SpanArgs& a, int n_cells, cudaStream_t s);
+// combine (attention.cpp:142-162) of each cell's n_parts states -> out rows
+// b*heads_q + hk*rows + r; optional log2-sum-exp; res_len (nullable) += 1
+cudaError_t launch_span_combine(const float* parts, int n_cells, int n_parts, int rows, int d,
+                                int heads_kv, int heads_q, float* out, float* out_lse,
+                                int* res_len, cudaStream_t s);
+cudaError_t launch_partitioned_rowmax(const float* s, int rows, int cols, int warp_n, float* out,
+                                      cudaStream_t st);
+
 // quant.hpp utilities (bdk_quantize_tile / bdk_dequantize_tile)
 cudaError_t launch_quantize_tile(const float* x, int rows, int d, int bits, int axis, int g,
                                  uint16_t* codes, uint32_t* params, cudaStream_t s);

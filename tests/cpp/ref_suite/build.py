@@ -11,9 +11,8 @@ Binaries go to paper_2503_18773_b200/lib/ref_suite/ (git-ignored; they travel
 to the GPU box with the tree).  Needs /root/reference (only in the build
 container); tests/test_ref_suite.py runs whatever was built.
 
-Not built: test_attention.cpp and test_bench.cpp exercise the CPU engine's
-internals (attend_tile, StagingBuffer, PartialOutput lists, run_bench),
-which the fused kernels replace.
+Not built: test_bench.cpp drives the reference's CPU benchmark harness
+(run_bench, CaseDriver, CSV output), a caller outside the hot path.
 """
 from __future__ import annotations
 
@@ -27,7 +26,7 @@ REF_TESTS = "/root/reference/proj/tests"
 OUT = os.path.join(ROOT, "paper_2503_18773_b200", "lib", "ref_suite")
 LIBDIR = os.path.join(ROOT, "paper_2503_18773_b200", "lib")
 ORACLE = os.path.join(ROOT, "oracle")
-SUITES = ["test_fp16", "test_layout", "test_quant", "test_config", "test_kvcache",
+SUITES = ["test_fp16", "test_layout", "test_quant", "test_config", "test_kvcache", "test_attention",
           "test_serialize", "test_oracle"]
 
 
