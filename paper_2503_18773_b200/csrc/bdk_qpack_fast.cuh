@@ -101,6 +101,15 @@ __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, ui
   // |q - x/s| <= 2^-22 q: a product farther than 4 * 2^-22 * (qmax + 1) from a
   // half-integer rounds like the exact quotient
   constexpr float TIE = 0.5f - 4.f * (1.f / 4194304.f) * (float)(1 << BITS);
+  // q + 1.5 * 2^23 lands in [2^23, 2^24), where the ulp is 1: the FADD rounds q
+  // to an integer (ties to even, as rintf) and leaves it in the low mantissa
+  // bits, so rint + float->int costs one FADD instead of two XU-pipe ops.  The
+  // exponent bits ride along through the shifted sums and are subtracted once.
+  constexpr float MAGIC = 12582912.f;
+  constexpr uint32_t MAGIC_BITS = 0x4B400000u;
+  uint32_t bias = 0;
+#pragma unroll
+  for (int p = 0; p < P; ++p) bias += MAGIC_BITS << (p * BITS);
   for (int item = threadIdx.x; item < SPLIT * CPT * (QF_D / 2); item += QF_THREADS) {
     const int sp = item / (CPT * (QF_D / 2));
     const int jl = (item / (QF_D / 2)) % CPT, cp = item % (QF_D / 2);
@@ -125,13 +134,18 @@ __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, ui
           const int t = tw + tok[p];
           if (TOKEN_PARAMS) pa = pb = fs[t];
           const float2 x = __half22float2(tile2[(size_t)t * 64 + cp]);
-          const float q0 = __fmul_rn(__fsub_rn(x.x, pa.y), pa.z);
-          const float q1 = __fmul_rn(__fsub_rn(x.y, pb.y), pb.z);
-          const float r0 = rintf(q0), r1 = rintf(q1);
+          // fmaxf maps a NaN quotient (a non-finite group) to code 0, as the
+          // reference's clamp + cast does on x86; in-group quotients are >= 0
+          const float q0 = fmaxf(__fmul_rn(__fsub_rn(x.x, pa.y), pa.z), 0.f);
+          const float q1 = fmaxf(__fmul_rn(__fsub_rn(x.y, pb.y), pb.z), 0.f);
+          const float t0m = __fadd_rn(q0, MAGIC), t1m = __fadd_rn(q1, MAGIC);
+          const float r0 = __fsub_rn(t0m, MAGIC), r1 = __fsub_rn(t1m, MAGIC);
           tie |= (fabsf(q0 - r0) > TIE) | (fabsf(q1 - r1) > TIE);
-          a0 += __float2uint_rn(r0) << (p * BITS);
-          a1 += __float2uint_rn(r1) << (p * BITS);
+          a0 += __float_as_uint(t0m) << (p * BITS);
+          a1 += __float_as_uint(t1m) << (p * BITS);
         }
+        a0 -= bias;
+        a1 -= bias;
         if (__any_sync(0xffffffffu, tie) && tie) {
           a0 = exact_word<BITS>(tile, fs, TOKEN_PARAMS, tw, 2 * cp, pa, G.interleave);
           a1 = exact_word<BITS>(tile, fs, TOKEN_PARAMS, tw, 2 * cp + 1, pb, G.interleave);
