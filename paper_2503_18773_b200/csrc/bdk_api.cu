@@ -984,7 +984,7 @@ void f32_to_f16_serial(const float* in, uint16_t* out, size_t n) {
 // large host tensors (e.g. b32 MHA: 1.5 MB of fp32 inputs per step) are
 // converted / copied by several host threads: a single core's memory
 // bandwidth would otherwise dominate the host-API step
-constexpr size_t kParallelHost = size_t(1) << 17;  // elements
+constexpr size_t kParallelHost = size_t(1) << 14;  // elements (back-to-back calls keep the pool warm)
 constexpr int kHostThreads = 8;
 
 void f32_to_f16_host(const float* in, uint16_t* out, size_t n) {
@@ -997,6 +997,37 @@ void f32_to_f16_host(const float* in, uint16_t* out, size_t n) {
   for (int t = 0; t < kHostThreads; ++t) {
     const size_t lo = std::min(n, (size_t)t * chunk), hi = std::min(n, lo + chunk);
     if (hi > lo) f32_to_f16_serial(in + lo, out + lo, hi - lo);
+  }
+}
+
+// q, k_new, v_new -> one contiguous fp16 staging run [q | k | v], one
+// parallel region for the three
+void f32_to_f16_host3(const float* q, size_t nq, const float* k, const float* v, size_t nk,
+                      uint16_t* out) {
+  const size_t n = nq + 2 * nk;
+  auto src = [&](size_t i, size_t& len) -> const float* {  // run containing element i
+    if (i < nq) return len = nq - i, q + i;
+    if (i < nq + nk) return len = nq + nk - i, k + (i - nq);
+    return len = n - i, v + (i - nq - nk);
+  };
+  auto convert = [&](size_t lo, size_t hi) {
+    while (lo < hi) {
+      size_t len;
+      const float* p = src(lo, len);
+      len = std::min(len, hi - lo);
+      f32_to_f16_serial(p, out + lo, len);
+      lo += len;
+    }
+  };
+  if (n < kParallelHost) {
+    convert(0, n);
+    return;
+  }
+  const size_t chunk = (n / kHostThreads + 7) & ~size_t(7);
+#pragma omp parallel for num_threads(kHostThreads) schedule(static)
+  for (int t = 0; t < kHostThreads; ++t) {
+    const size_t lo = std::min(n, (size_t)t * chunk), hi = std::min(n, lo + chunk);
+    convert(lo, hi);
   }
 }
 
@@ -1034,9 +1065,7 @@ bdk_status bdk_decode_step_host(bdk_cache* c, const bdk_attn_config* cfg, const 
   if (s) return s;
   BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
   uint16_t* hin = static_cast<uint16_t*>(c->h_stage);
-  f32_to_f16_host(q, hin, nq);
-  f32_to_f16_host(k_new, hin + nq, nk);
-  f32_to_f16_host(v_new, hin + nq + nk, nk);
+  f32_to_f16_host3(q, nq, k_new, v_new, nk, hin);
   __half* dh = static_cast<__half*>(c->d_stage);
   float* hout = reinterpret_cast<float*>(static_cast<uint8_t*>(c->h_stage) + out_off);
   // small outputs (<= 256 KiB) are stored by the kernel over PCIe into the
