@@ -1075,7 +1075,15 @@ bdk_status bdk_decode_step_host(bdk_cache* c, const bdk_attn_config* cfg, const 
   const bool zc = zc_env >= 0 ? zc_env != 0 : nq * 4 <= (256u << 10);
   float* dout = zc ? hout : reinterpret_cast<float*>(static_cast<uint8_t*>(c->d_stage) + out_off);
   cudaStream_t st = 0;
-  BDK_CUDA(cudaMemcpyAsync(dh, hin, n_in * 2, cudaMemcpyHostToDevice, st), "H2D");
+  // small inputs cross PCIe in a kernel the decode kernel overlaps its start
+  // with (C5: +8% e2e); large ones stream faster on the copy engine (C3).
+  // Staging buffers are padded past n_in, so the 16-byte round-up stays inside.
+  if (n_in * 2 <= (256u << 10)) {
+    BDK_CUDA(bdk::launch_stage_in(hin, dh, n_in * 2, st), "H2D stage-in");
+    c->launches += 1;
+  } else {
+    BDK_CUDA(cudaMemcpyAsync(dh, hin, n_in * 2, cudaMemcpyHostToDevice, st), "H2D");
+  }
   s = run_decode(c, cfg, dh, dh + nq, dh + nq + nk, dout, nullptr, 0, 1 << 30, st);
   if (s) return s;
   if (!zc) BDK_CUDA(cudaMemcpyAsync(hout, dout, nq * 4, cudaMemcpyDeviceToHost, st), "D2H");

@@ -117,6 +117,18 @@ __global__ void __launch_bounds__(256) flush_full_kernel(DevCache c) {
   }
 }
 
+// Host-API step inputs: pinned (mapped) host staging -> device, as a kernel
+// rather than a copy-engine transfer so that the decode kernel, launched as its
+// programmatic dependent, starts streaming packed blocks while the inputs are
+// still crossing PCIe (it reads them only after griddepcontrol.wait).
+__global__ void __launch_bounds__(256) stage_in_kernel(const uint4* __restrict__ src,
+                                                       uint4* __restrict__ dst, size_t n16) {
+  pdl_launch_dependents();
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 // packed_tile dequant: blocks [blk0, blk0 + gridDim.x) of a cell -> fp16 rows
 __global__ void dequant_kernel(DevCache c, int cell, int blk0, __half* k_out, __half* v_out) {
   const Geom& G = c.G;
@@ -922,6 +934,15 @@ cudaError_t launch_flush_full(const DevCache& c, cudaStream_t s) {
     case 16: return flush_full_bits<16>(c, s);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_stage_in(const void* src_host, void* dst, size_t bytes, cudaStream_t s) {
+  const size_t n16 = (bytes + 15) / 16;
+  if (n16 == 0) return cudaSuccess;
+  const int grid = static_cast<int>(std::min<size_t>((n16 + 255) / 256, 148));
+  stage_in_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(src_host),
+                                        static_cast<uint4*>(dst), n16);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_dequant(const DevCache& c, int cell, int blk0, int nblk, __half* k_out,

@@ -90,6 +90,9 @@ cudaError_t launch_append(const DevCache& c, int cell, const __half* k_row, cons
 cudaError_t launch_flush(const DevCache& c, int cell, cudaStream_t s);
 cudaError_t launch_build(const DevCache& c, int cell, cudaStream_t s);  // pack, no commit
 cudaError_t launch_decode(const DevCache& c, const DecodeArgs& a, cudaStream_t s);
+// copy bytes (rounded up to 16) from mapped pinned host memory to the device;
+// a PDL primary for the decode launch that follows
+cudaError_t launch_stage_in(const void* src_host, void* dst, size_t bytes, cudaStream_t s);
 // dequantize blocks [blk0, blk0+nblk) of a cell into fp16 [nblk*n_r][d] rows
 cudaError_t launch_dequant(const DevCache& c, int cell, int blk0, int nblk, __half* k_out,
                            __half* v_out, cudaStream_t s);
