@@ -272,7 +272,10 @@ class OracleCache:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib().orc_cache_destroy(h)
+            try:  # module globals may already be gone at interpreter exit
+                lib().orc_cache_destroy(h)
+            except Exception:
+                pass
             self._h = None
 
     def packed_len(self, b, h):
