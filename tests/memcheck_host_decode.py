@@ -1,5 +1,5 @@
 # dev check: host decode_step (fast kernel + PDL stage-in) vs the oracle, small enough for
-# compute-sanitizer memcheck:  compute-sanitizer --tool memcheck python tools/memcheck_host_decode.py
+# compute-sanitizer memcheck:  compute-sanitizer --tool memcheck python tests/memcheck_host_decode.py
 import numpy as np, sys
 sys.path.insert(0, '/root/repo')
 from paper_2503_18773_b200 import bitkv as bk
