@@ -313,7 +313,8 @@ def run_ours(args, w, world, rank, local):
             (args.e2e_steps, w["batch"], w["hkv"], D)).astype(np.float16).astype(np.float32)
         hv = np.random.default_rng(rank + 2).standard_normal(
             (args.e2e_steps, w["batch"], w["hkv"], D)).astype(np.float16).astype(np.float32)
-        bk.decode_step(reps[0], cfg, hq[0], hk[0], hv[0])  # staging allocation
+        hout = np.empty((w["batch"], w["hq"], D), np.float32)  # reused output (decode_step(out=))
+        bk.decode_step(reps[0], cfg, hq[0], hk[0], hv[0], out=hout)  # staging allocation
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -327,7 +328,7 @@ def run_ours(args, w, world, rank, local):
                              ("k_packed_payload_bytes", "v_packed_payload_bytes",
                               "params_bytes"))
             t0 = time.perf_counter()
-            res = bk.decode_step(r, cfg, hq[i], hk[i], hv[i])
+            res = bk.decode_step(r, cfg, hq[i], hk[i], hv[i], out=hout)
             e2e_s += time.perf_counter() - t0
         e2e_ms = e2e_s * 1e3
         assert np.isfinite(res.data).all()

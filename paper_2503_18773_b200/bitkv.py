@@ -675,7 +675,9 @@ def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None)
     """decode_step (attention.hpp:87-88, attention.cpp:164-242).
 
     CUDA fp16 tensors in -> CUDA fp32 ``out`` (stream-ordered, no sync).
-    Host arrays in -> numpy out via the host C-ABI entry (H2D/D2H inside)."""
+    Host arrays in -> numpy out via the host C-ABI entry (H2D/D2H inside);
+    ``out`` may then be a C-contiguous float32 numpy array of q's shape to
+    reuse across steps."""
     c = cfg._c()
     shape_q = (cfg.batch, cfg.heads_q, cfg.head_dim)
     shape_kv = (cfg.batch, cfg.heads_kv, cfg.head_dim)
@@ -688,7 +690,11 @@ def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None)
             validate_config(cfg)
             raise ShapeError("decode_step: q must be [batch, heads_q, d], k_new/v_new "
                              "[batch, heads_kv, d]")
-        o = np.empty(shape_q, np.float32)
+        if isinstance(out, np.ndarray) and out.shape == shape_q and out.dtype == np.float32 \
+                and out.flags.c_contiguous and out.flags.writeable:
+            o = out
+        else:
+            o = np.empty(shape_q, np.float32)
         _check(_L.load().bdk_decode_step_host(cache.handle(), C.byref(c), _addr(qh), _addr(kh),
                                               _addr(vh), _addr(o)))
         return AttnOutput(cfg.batch, cfg.heads_q, cfg.head_dim, o)
