@@ -302,6 +302,11 @@ def test_host_api_matches_device_api():
                         torch.from_numpy(kn).cuda().half(),
                         torch.from_numpy(vn).cuda().half()).data.cpu().numpy()
     assert np.array_equal(oh, od)
+    # a caller-provided output array is filled in place and reused
+    c2 = gpu_cache(c, k, v)
+    buf = np.full((1, 8, D), np.nan, np.float32)
+    res = bk.decode_step(c2, cfg, q, kn, vn, out=buf)
+    assert res.data is buf and np.array_equal(buf, oh)
 
 
 # ------------------------------------------- golden fixtures (reference engine)
