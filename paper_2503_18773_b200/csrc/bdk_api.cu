@@ -357,7 +357,17 @@ bdk_status run_decode_span(bdk_cache* c, const bdk_attn_config* cfg, const void*
   a.d = d;
   a.residual = no_res ? 0 : 1;
   a.tile_n = static_cast<int>(cfg->tile_n);
-  a.splits = static_cast<int>(cfg->num_splits);
+  // the reference's num_splits, raised so that no CTA walks more than 4
+  // tiles (a CTA's walk is sequential; results are split-invariant within
+  // the reference's 1e-5, test_attention.cpp:312-340)
+  {
+    int nblk = 0;
+    for (int i = 0; i < cells; ++i) nblk = std::max(nblk, c->packed_blocks[i]);
+    const long long lo = std::max(0, blk_begin), hi = std::min<long long>(blk_end, nblk);
+    const long long toks = std::max(0LL, hi - lo) * c->dev.G.n_r;
+    const long long tiles = (toks + cfg->tile_n - 1) / cfg->tile_n;
+    a.splits = static_cast<int>(std::max<long long>(cfg->num_splits, std::min(1024LL, (tiles + 3) / 4)));
+  }
   a.blk_begin = std::max(0, blk_begin);
   a.blk_end = blk_end;
   a.warp_n = static_cast<int>(cfg->warp_n);
