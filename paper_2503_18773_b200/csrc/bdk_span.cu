@@ -11,11 +11,11 @@
 // attention.cpp:52-90).  Every dot product, row sum and P.V sum runs in the
 // reference's order with unfused fp32 operations (__fmul_rn/__fadd_rn, no
 // FMA contraction), so the one difference from the host is expf (CUDA,
-// <= 2 ulp) against libm.  q, the score tile and the per-row rescale factors
-// sit in shared memory; the partial state (o, m, l) stays in the parts
-// buffer, each element owned by one thread across tiles; K/V elements are
-// read -- and dequantized from the packed block records -- where they are
-// used.  This path is latency-bound by construction; the hot path's
+// <= 2 ulp) against libm.  q, the score tile, the per-row rescale factors,
+// the running P.V sums and a 32-token chunk of K or V rows (dequantized once
+// from the packed block records) sit in shared memory; the partial state
+// (o, m, l) stays in the parts buffer, each element owned by one thread
+// across tiles.  This path is latency-bound by construction; the hot path's
 // throughput lives in the fast kernels.
 #include <cfloat>
 
@@ -48,22 +48,38 @@ __device__ __forceinline__ float span_kv(const SpanCtx& x, int t, int ch, int wh
   return __half2float(packed_elem(G, rec, t % G.n_r, ch, which));
 }
 
+// K/V rows staged per chunk of the tile: dequantized once into shared memory
+// (row stride d + 1, so the S loop's strided rows hit distinct banks)
+constexpr int kSpanChunk = 32;
+
+__device__ __forceinline__ void stage_rows(const SpanCtx& x, int t0, int m, int d, int which,
+                                           float* kv) {
+  for (int i = threadIdx.x; i < m * d; i += blockDim.x) {
+    const int j = i / d, c = i % d;
+    kv[j * (d + 1) + c] = span_kv(x, t0 + j, c, which);
+  }
+}
+
 // online softmax over tokens [t_begin, t_end) in tiles of tile_n
 __device__ void span_walk(const SpanCtx& x, const float* q, int rows, int d, float scale,
                           int tile_n, int t_begin, int t_end, float* o, float* m, float* l,
-                          float* s, float* resc) {
+                          float* s, float* resc, float* pacc, float* kv) {
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int t0 = t_begin; t0 < t_end; t0 += tile_n) {
     const int n = min(tile_n, t_end - t0);
     // S = scale * q k^T, sequential over channels
-    for (int i = tid; i < rows * n; i += nt) {
-      const int r = i / n, j = i % n;
-      float acc = 0.f;
-      for (int c = 0; c < d; ++c)
-        acc = __fadd_rn(acc, __fmul_rn(q[r * d + c], span_kv(x, t0 + j, c, 0)));
-      s[r * n + j] = __fmul_rn(acc, scale);
+    for (int c0 = 0; c0 < n; c0 += kSpanChunk) {
+      const int mc = min(kSpanChunk, n - c0);
+      stage_rows(x, t0 + c0, mc, d, 0, kv);
+      __syncthreads();
+      for (int i = tid; i < rows * mc; i += nt) {
+        const int r = i / mc, j = i % mc;
+        float acc = 0.f;
+        for (int c = 0; c < d; ++c) acc = __fadd_rn(acc, __fmul_rn(q[r * d + c], kv[j * (d + 1) + c]));
+        s[r * n + c0 + j] = __fmul_rn(acc, scale);
+      }
+      __syncthreads();
     }
-    __syncthreads();
     // row max (a partitioned max is the same number), rescale, P, row sum
     for (int r = tid; r < rows; r += nt) {
       float tm = -INFINITY;
@@ -81,15 +97,24 @@ __device__ void span_walk(const SpanCtx& x, const float* q, int rows, int d, flo
       m[r] = m_new;
       resc[r] = rs;
     }
-    __syncthreads();
-    // O' = P V + rescale * O, sequential over the tile's tokens
-    for (int i = tid; i < rows * d; i += nt) {
-      const int r = i / d, c = i % d;
-      float acc = 0.f;
-      for (int j = 0; j < n; ++j)
-        acc = __fadd_rn(acc, __fmul_rn(s[r * n + j], span_kv(x, t0 + j, c, 1)));
-      o[i] = __fadd_rn(acc, __fmul_rn(resc[r], o[i]));
+    for (int i = tid; i < rows * d; i += nt) pacc[i] = 0.f;
+    // O' = P V + rescale * O, sequential over the tile's tokens (the running
+    // sum carries across chunks, so the order is the reference's)
+    for (int c0 = 0; c0 < n; c0 += kSpanChunk) {
+      const int mc = min(kSpanChunk, n - c0);
+      __syncthreads();
+      stage_rows(x, t0 + c0, mc, d, 1, kv);
+      __syncthreads();
+      for (int i = tid; i < rows * d; i += nt) {
+        const int r = i / d, c = i % d;
+        float acc = pacc[i];
+        for (int j = 0; j < mc; ++j)
+          acc = __fadd_rn(acc, __fmul_rn(s[r * n + c0 + j], kv[j * (d + 1) + c]));
+        pacc[i] = acc;
+      }
     }
+    __syncthreads();
+    for (int i = tid; i < rows * d; i += nt) o[i] = __fadd_rn(pacc[i], __fmul_rn(resc[i / d], o[i]));
     __syncthreads();
   }
 }
@@ -99,9 +124,12 @@ __global__ void __launch_bounds__(kSpanThreads) span_parts_kernel(SpanArgs a) {
   const int rows = a.rows, d = a.d;
   const int cell = a.cell0 + blockIdx.y, part = blockIdx.x;
   const Geom& G = a.c.G;
+  const int tile_max = a.source == kSpanFp32 ? a.len32 : max(a.tile_n, G.n_r);
   float* q = sm;
   float* resc = q + rows * d;
-  float* s = resc + rows;
+  float* pacc = resc + rows;
+  float* kv = pacc + rows * d;
+  float* s = kv + kSpanChunk * (d + 1);
   float* st = a.parts + ((size_t)blockIdx.y * a.n_parts + part) * rows * (d + 2);
   float* o = st;
   float* m = st + rows * d;
@@ -156,7 +184,8 @@ __global__ void __launch_bounds__(kSpanThreads) span_parts_kernel(SpanArgs a) {
     t_end = count ? min(lo + (first + count) * a.tile_n, hi) : t_begin;
   }
   __syncthreads();
-  span_walk(x, q, rows, d, a.scale, tile, t_begin, t_end, o, m, l, s, resc);
+  (void)tile_max;
+  span_walk(x, q, rows, d, a.scale, tile, t_begin, t_end, o, m, l, s, resc, pacc, kv);
 }
 
 __global__ void __launch_bounds__(256)
@@ -201,7 +230,7 @@ __global__ void partitioned_rowmax_kernel(const float* s, int rows, int cols, in
 }  // namespace
 
 size_t span_smem_bytes(int rows, int d, int tile) {
-  return (size_t)rows * (d + 1 + tile) * sizeof(float);
+  return ((size_t)rows * (2 * d + 1 + tile) + (size_t)kSpanChunk * (d + 1)) * sizeof(float);
 }
 
 cudaError_t launch_span_parts(const SpanArgs& a, int n_cells, cudaStream_t s) {
