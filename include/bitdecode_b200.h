@@ -221,7 +221,12 @@ BDK_API bdk_status bdk_combine_host(const float* o, const float* m, const float*
                                     uint32_t n_parts, uint32_t rows, uint32_t d, float* out,
                                     int32_t device);
 
-/* 0 = fast (fp16 P), 1 = precise PV (P = P_hi + P_lo) */
+/* Decode numerics of a cache.  1 = precise (the default for every new or
+ * loaded cache): bit-faithful round_f16(code*scale + zero) dequant and the
+ * P = P_hi + P_lo split PV, within the reference's own 1e-5 decode tolerance
+ * (proj/tests/test_attention.cpp:350-441).  0 = fast: scales folded into Q and
+ * P, fp16 P (the throughput kernel; rel-L2 ~1e-3), an
+ * explicit opt-in. */
 BDK_API bdk_status bdk_set_precise(bdk_cache* cache, int precise);
 
 /* --------------------------------------------------------- readback/IO */

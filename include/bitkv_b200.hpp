@@ -686,8 +686,9 @@ class KVCache {  // kvcache.hpp:103-189, cache resident in HBM
     detail::check(bdk_memory(h_, m));
     return Memory{m[0], m[1], m[2], m[3]};
   }
-  // fp16 P (false, default) or the hi/lo split PV with bit-faithful dequant
-  // (true): the reference's own 1e-5 tolerances
+  // precise (true, the default: bit-faithful dequant + hi/lo split PV, the
+  // reference's own 1e-5 tolerances) or fast (false: folded
+  // scales, fp16 P -- the throughput kernel, an explicit opt-in)
   void set_precise(bool precise) { detail::check(bdk_set_precise(h_, precise ? 1 : 0)); }
   // empty every cell, keeping the device arena (a fresh KVCache of the same
   // geometry without reallocating)

@@ -381,7 +381,7 @@ class KVCache:
     def __init__(self, batch: int, heads_kv: int, head_dim: int, warp_n: int,
                  spec: QuantSpec | None = None, backend: CacheBackend = CacheBackend.Contiguous,
                  page_size: int = 16, max_pages: int = 0, interleave: bool = True, *,
-                 max_tokens: int = 1 << 16, device: int = 0):
+                 max_tokens: int = 1 << 16, device: int = 0, precise: bool = True):
         spec = spec or QuantSpec()
         self._h = None
         if backend == CacheBackend.Paged:
@@ -399,6 +399,8 @@ class KVCache:
         info = _L.CacheInfo()
         _check(_L.load().bdk_cache_get_info(self._h, C.byref(info)))
         self.info = info
+        if not precise:
+            self.set_precise(False)
 
     @classmethod
     def _adopt(cls, handle, header: bytes, device: int) -> "KVCache":
@@ -610,7 +612,10 @@ class KVCache:
         return n.value
 
     def set_precise(self, precise: bool) -> None:
-        """fp16 P (False) or P_hi + P_lo split PV (True), SURVEY.md F4."""
+        """Decode numerics.  True (the default of every cache): bit-faithful
+        dequant + P_hi + P_lo split PV, the reference's 1e-5 contract
+        (test_attention.cpp:350-441).  False: the fast throughput kernel
+        (folded scales, fp16 P; an explicit opt-in), SURVEY.md F4."""
         _check(_L.load().bdk_set_precise(self._h, 1 if precise else 0))
 
 
@@ -690,11 +695,14 @@ def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None)
             validate_config(cfg)
             raise ShapeError("decode_step: q must be [batch, heads_q, d], k_new/v_new "
                              "[batch, heads_kv, d]")
-        if isinstance(out, np.ndarray) and out.shape == shape_q and out.dtype == np.float32 \
+        if out is None:
+            o = np.empty(shape_q, np.float32)
+        elif isinstance(out, np.ndarray) and out.shape == shape_q and out.dtype == np.float32 \
                 and out.flags.c_contiguous and out.flags.writeable:
             o = out
         else:
-            o = np.empty(shape_q, np.float32)
+            raise ShapeError(f"decode_step: out must be a writable C-contiguous float32 array "
+                             f"of shape {shape_q}")
         _check(_L.load().bdk_decode_step_host(cache.handle(), C.byref(c), _addr(qh), _addr(kh),
                                               _addr(vh), _addr(o)))
         return AttnOutput(cfg.batch, cfg.heads_q, cfg.head_dim, o)
@@ -703,13 +711,26 @@ def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None)
         validate_config(cfg)
         raise ShapeError("decode_step: q must be [batch, heads_q, d], k_new/v_new "
                          "[batch, heads_kv, d]")
-    qd, kd, vd = (_as_f16_cuda(x) for x in (q, k_new, v_new))
+    qd, kd, vd = (_as_f16_cuda(x, device=cache._device) for x in (q, k_new, v_new))
     if out is None:
-        out = torch.empty(shape_q, dtype=torch.float32, device=q.device)
+        out = torch.empty(shape_q, dtype=torch.float32, device=qd.device)
+    else:
+        _check_f32_out(out, shape_q, cache, "out")
     _check(_L.load().bdk_decode_step(cache.handle(), C.byref(c), C.c_void_p(qd.data_ptr()),
                                      C.c_void_p(kd.data_ptr()), C.c_void_p(vd.data_ptr()),
                                      C.c_void_p(out.data_ptr()), _stream_ptr()))
     return AttnOutput(cfg.batch, cfg.heads_q, cfg.head_dim, out)
+
+
+def _check_f32_out(t, shape, cache: KVCache, name: str) -> None:
+    """A caller-provided device output must be a contiguous fp32 CUDA tensor
+    of the exact shape on the cache's GPU (the kernels write it blindly)."""
+    ok = (torch is not None and isinstance(t, torch.Tensor) and t.is_cuda
+          and t.dtype == torch.float32 and t.is_contiguous() and tuple(t.shape) == tuple(shape)
+          and t.device.index == cache._device)
+    if not ok:
+        raise ShapeError(f"{name} must be a contiguous float32 CUDA tensor of shape "
+                         f"{tuple(shape)} on cuda:{cache._device}")
 
 
 class DecodeStepper:
@@ -768,13 +789,21 @@ def decode_partial(cache: KVCache, cfg: AttentionConfig, q, k_new=None, v_new=No
     partial output [batch, heads_q, d] and its log2-sum-exp [batch, heads_q].
     k_new/v_new None: attend only (no append, no commit)."""
     c = cfg._c()
-    qd = _as_f16_cuda(q)
-    kd = _as_f16_cuda(k_new) if k_new is not None else None
-    vd = _as_f16_cuda(v_new) if v_new is not None else None
-    o = out if out is not None else torch.empty((cfg.batch, cfg.heads_q, cfg.head_dim),
-                                                dtype=torch.float32, device=qd.device)
+    dev = cache._device
+    qd = _as_f16_cuda(q, (cfg.batch, cfg.heads_q, cfg.head_dim), dev)
+    shape_kv = (cfg.batch, cfg.heads_kv, cfg.head_dim)
+    kd = _as_f16_cuda(k_new, shape_kv, dev) if k_new is not None else None
+    vd = _as_f16_cuda(v_new, shape_kv, dev) if v_new is not None else None
+    if out is None:
+        o = torch.empty((cfg.batch, cfg.heads_q, cfg.head_dim), dtype=torch.float32,
+                        device=qd.device)
+    else:
+        _check_f32_out(out, (cfg.batch, cfg.heads_q, cfg.head_dim), cache, "out")
+        o = out
     if lse is None:
         lse = torch.empty((cfg.batch, cfg.heads_q), dtype=torch.float32, device=qd.device)
+    else:
+        _check_f32_out(lse, (cfg.batch, cfg.heads_q), cache, "lse")
     _check(_L.load().bdk_decode_partial(
         cache.handle(), C.byref(c), C.c_void_p(qd.data_ptr()),
         C.c_void_p(kd.data_ptr()) if kd is not None else None,

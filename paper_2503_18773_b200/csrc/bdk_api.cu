@@ -30,7 +30,7 @@ struct bdk_cache {
   bdk_cache_desc desc{};
   int device = 0;
   int num_sms = 148;
-  int precise = 0;
+  int precise = 1;  // the reference's 1e-5 contract unless the caller opts into fast
   uint32_t kp_u16 = 0, vp_u16 = 0, wpb = 0;
   std::vector<int> packed_blocks, res_len;  // host mirror
   // decode workspace
@@ -72,6 +72,23 @@ bdk_status cuda_fail(cudaError_t e, const char* where) {
   g_err = std::string(where) + ": " + cudaGetErrorString(e);
   return BDK_CUDA_ERROR;
 }
+
+// Makes `dev` current for the scope of one C-ABI call and restores the
+// caller's device on exit: every allocation and launch of a cache lands on the
+// cache's own GPU, and a call never changes the calling thread's device.
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DevGuard(const DevGuard&) = delete;
+  DevGuard& operator=(const DevGuard&) = delete;
+};
 
 #define BDK_CUDA(call, where)                  \
   do {                                         \
@@ -211,7 +228,7 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
   const int cells = static_cast<int>(c->desc.batch * c->desc.heads_kv);
   const int ng = static_cast<int>(cfg->heads_q / cfg->heads_kv);
   const Geom& G = c->dev.G;
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   if (c->fast_ng != ng) {
     c->fast_ctas_per_sm = bdk::fast_decode_ctas_per_sm(G, ng);
     c->fast_ng = ng;
@@ -339,8 +356,10 @@ bdk_status ensure_span(bdk_cache* c, size_t floats) {
 
 // decode_step on the span path (bdk_span.cu): the reference's own
 // decomposition -- residual window (with the appended token) as part 0, then
-// cfg->num_splits packed splits of cfg->tile_n tiles -- combined in that
-// order, then the flush of any residual the step filled
+// packed splits of cfg->tile_n tiles by the reference's split rule -- combined
+// in that order, then the flush of any residual the step filled.  The split
+// count is cfg->num_splits raised so that no CTA walks more than 4 tiles
+// (capped at 1024 splits and by a 256 MiB partial-state budget).
 bdk_status run_decode_span(bdk_cache* c, const bdk_attn_config* cfg, const void* q,
                            const void* k_new, const void* v_new, float* out, float* lse,
                            int blk_begin, int blk_end, cudaStream_t stream, bool no_res) {
@@ -366,7 +385,10 @@ bdk_status run_decode_span(bdk_cache* c, const bdk_attn_config* cfg, const void*
     const long long lo = std::max(0, blk_begin), hi = std::min<long long>(blk_end, nblk);
     const long long toks = std::max(0LL, hi - lo) * c->dev.G.n_r;
     const long long tiles = (toks + cfg->tile_n - 1) / cfg->tile_n;
-    a.splits = static_cast<int>(std::max<long long>(cfg->num_splits, std::min(1024LL, (tiles + 3) / 4)));
+    const long long per_split = (long long)cells * ng * (d + 2);  // floats of one split
+    const long long budget = std::max(1LL, (64LL << 20) / std::max(1LL, per_split) - 1);
+    const long long raised = std::min({1024LL, (tiles + 3) / 4, budget});
+    a.splits = static_cast<int>(std::max<long long>(cfg->num_splits, raised));
   }
   a.blk_begin = std::max(0, blk_begin);
   a.blk_end = blk_end;
@@ -375,7 +397,7 @@ bdk_status run_decode_span(bdk_cache* c, const bdk_attn_config* cfg, const void*
   bdk_status s = ensure_span(c, (size_t)cells * a.n_parts * ng * (d + 2));
   if (s) return s;
   a.parts = c->span_parts;
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   BDK_CUDA(bdk::launch_span_parts(a, cells, stream), "span launch");
   BDK_CUDA(bdk::launch_span_combine(c->span_parts, cells, a.n_parts, ng, d,
                                     static_cast<int>(c->desc.heads_kv),
@@ -404,6 +426,7 @@ bdk_status run_decode_span(bdk_cache* c, const bdk_attn_config* cfg, const void*
 bdk_status run_decode(bdk_cache* c, const bdk_attn_config* cfg, const void* q, const void* k_new,
                       const void* v_new, float* out, float* lse, int blk_begin, int blk_end,
                       cudaStream_t stream, bool no_res = false) {
+  DevGuard dev_guard_(c->device);  // workspaces and launches on the cache's GPU
   const int cells = static_cast<int>(c->desc.batch * c->desc.heads_kv);
   if (!exact_ok(c, cfg))
     return run_decode_span(c, cfg, q, k_new, v_new, out, lse, blk_begin, blk_end, stream, no_res);
@@ -445,7 +468,6 @@ bdk_status run_decode(bdk_cache* c, const bdk_attn_config* cfg, const void* q, c
   a.skip_residual = no_res ? 1 : 0;
   a.precise = c->precise;
   a.sm_scale_log2 = (1.0f / std::sqrt(static_cast<float>(cfg->head_dim))) * bdk::kLog2e;
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
   {
     bdk_status st = next_events(c, &a.ev_begin, &a.ev_end);
     if (st) return st;
@@ -543,7 +565,10 @@ bdk_status bdk_cache_create(const bdk_cache_desc* d, bdk_cache** out) {
   const size_t cells = (size_t)d->batch * d->heads_kv;
   c->packed_blocks.assign(cells, 0);
   c->res_len.assign(cells, 0);
-  cudaError_t e = cudaSetDevice(d->device);
+  DevGuard dev_guard_(d->device);
+  int n_dev = 0;
+  cudaError_t e = cudaGetDeviceCount(&n_dev);
+  if (e == cudaSuccess && (d->device < 0 || d->device >= n_dev)) e = cudaErrorInvalidDevice;
   if (e == cudaSuccess)
     e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, d->device);
   if (e == cudaSuccess)
@@ -564,7 +589,7 @@ bdk_status bdk_cache_create(const bdk_cache_desc* d, bdk_cache** out) {
 
 bdk_status bdk_cache_destroy(bdk_cache* c) {
   if (!c) return BDK_OK;
-  cudaSetDevice(c->device);
+  DevGuard dev_guard_(c->device);
   cudaFree(c->dev.records);
   cudaFree(c->dev.res_k);
   cudaFree(c->dev.res_v);
@@ -619,7 +644,7 @@ bdk_status bdk_prefill(bdk_cache* c, uint32_t b, uint32_t h, const void* k, cons
   const int nb = static_cast<int>(len / c->dev.G.n_r);
   if (nb > c->dev.G.max_blocks) return fail(BDK_CAPACITY_ERROR, "prefill exceeds max_tokens");
   if (len > 0 && (!k || !v)) return fail(BDK_INVALID_ARGUMENT, "null k/v");
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   c->launches += 1;
   c->blocks_written = true;
   BDK_CUDA(bdk::launch_prefill(c->dev, static_cast<const __half*>(k),
@@ -634,7 +659,7 @@ bdk_status bdk_prefill(bdk_cache* c, uint32_t b, uint32_t h, const void* k, cons
 bdk_status bdk_cache_reset(bdk_cache* c, void* stream) {
   if (!c) return fail(BDK_INVALID_ARGUMENT, "null cache");
   const size_t cells = c->res_len.size();
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   BDK_CUDA(cudaMemsetAsync(c->dev.packed_blocks, 0, cells * sizeof(int), as_stream(stream)),
            "reset packed_blocks");
   BDK_CUDA(cudaMemsetAsync(c->dev.res_len, 0, cells * sizeof(int), as_stream(stream)),
@@ -654,7 +679,7 @@ bdk_status bdk_prefill_all(bdk_cache* c, const void* k, const void* v, uint32_t 
   const int nb = static_cast<int>(len / c->dev.G.n_r);
   if (nb > c->dev.G.max_blocks) return fail(BDK_CAPACITY_ERROR, "prefill exceeds max_tokens");
   const int cells = static_cast<int>(c->res_len.size());
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   c->launches += 1;
   c->blocks_written = true;
   BDK_CUDA(bdk::launch_prefill(c->dev, static_cast<const __half*>(k),
@@ -675,7 +700,7 @@ bdk_status bdk_append_token(bdk_cache* c, uint32_t b, uint32_t h, const void* k,
   const int i = cell_of(c, b, h);
   if (c->res_len[i] == c->dev.G.n_r)
     return fail(BDK_CAPACITY_ERROR, "residual is full; flush before appending");
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   c->launches += 1;
   BDK_CUDA(bdk::launch_append(c->dev, i, static_cast<const __half*>(k),
                               static_cast<const __half*>(v), as_stream(stream)),
@@ -693,7 +718,7 @@ bdk_status bdk_flush_residual(bdk_cache* c, uint32_t b, uint32_t h, void* stream
                                      std::to_string(c->res_len[i]));
   if (c->packed_blocks[i] >= c->dev.G.max_blocks)
     return fail(BDK_CAPACITY_ERROR, "cache arena full (raise max_tokens)");
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   c->launches += 1;
   BDK_CUDA(bdk::launch_flush(c->dev, i, as_stream(stream)), "flush launch");
   c->blocks_written = true;
@@ -784,7 +809,7 @@ bdk_status bdk_attend_tile_host(float* o, float* m, float* l, uint32_t rows, uin
   if (rows == 0 || d == 0 || tile_n == 0) return BDK_OK;
   bdk_status s = span_fits(rows, d, tile_n);
   if (s) return s;
-  BDK_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  DevGuard dev_guard_(device);
   DevF bq, bk, bv, bs;
   BDK_CUDA(bq.alloc((size_t)rows * d), "cudaMalloc");
   BDK_CUDA(bk.alloc((size_t)tile_n * d), "cudaMalloc");
@@ -820,7 +845,7 @@ bdk_status bdk_partitioned_rowmax_host(const float* sc, uint32_t rows, uint32_t 
                 "partitioned_rowmax: cols must divide evenly across warp_n partitions");
   if (!sc || !out) return fail(BDK_INVALID_ARGUMENT, "null argument");
   if (rows == 0) return BDK_OK;
-  BDK_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  DevGuard dev_guard_(device);
   DevF bs, bo;
   BDK_CUDA(bs.alloc((size_t)rows * cols), "cudaMalloc");
   BDK_CUDA(bo.alloc(rows), "cudaMalloc");
@@ -841,7 +866,7 @@ bdk_status bdk_residual_attend_host(const bdk_cache* c, uint32_t b, uint32_t h, 
   if (q_rows == 0) return BDK_OK;
   const uint32_t d = c->desc.head_dim;
   if ((s = span_fits(q_rows, d, c->dev.G.n_r))) return s;
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   DevF bq, bs;
   BDK_CUDA(bq.alloc((size_t)q_rows * d), "cudaMalloc");
   BDK_CUDA(bs.alloc((size_t)q_rows * (d + 2)), "cudaMalloc");
@@ -881,7 +906,7 @@ bdk_status bdk_packed_attend_host(const bdk_cache* c, uint32_t b, uint32_t h, co
   // splits past the tile count are empty (attention.cpp:124-130) and omitted
   const uint64_t n_tiles = (plen + tile_n - 1) / tile_n;
   const uint32_t splits = (uint32_t)std::min<uint64_t>(std::max<uint32_t>(1, num_splits), n_tiles);
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   DevF bq, bs;
   const size_t stride = (size_t)q_rows * (d + 2);
   BDK_CUDA(bq.alloc((size_t)q_rows * d), "cudaMalloc");
@@ -914,7 +939,7 @@ bdk_status bdk_combine_host(const float* o, const float* m, const float* l, uint
   if (n_parts == 0) return fail(BDK_EMPTY_INPUT, "combine: no partial outputs");
   if (!o || !m || !l || !out) return fail(BDK_INVALID_ARGUMENT, "null argument");
   if (rows == 0 || d == 0) return BDK_OK;
-  BDK_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  DevGuard dev_guard_(device);
   const size_t stride = (size_t)rows * (d + 2);
   DevF bs, bo;
   BDK_CUDA(bs.alloc(stride * n_parts), "cudaMalloc");
@@ -1071,9 +1096,9 @@ bdk_status bdk_decode_step_host(bdk_cache* c, const bdk_attn_config* cfg, const 
   // staging layout (host and device alike): fp16 [q | k | v], fp32 out (128-B aligned)
   const size_t out_off = (n_in * 2 + 127) & ~size_t(127);
   const size_t bytes = out_off + nq * 4;
+  DevGuard dev_guard_(c->device);
   s = ensure_stage(c, bytes);
   if (s) return s;
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
   uint16_t* hin = static_cast<uint16_t*>(c->h_stage);
   f32_to_f16_host3(q, nq, k_new, v_new, nk, hin);
   __half* dh = static_cast<__half*>(c->d_stage);
@@ -1108,7 +1133,7 @@ bdk_status bdk_prefill_host(bdk_cache* c, uint32_t b, uint32_t h, const uint16_t
   if (s) return s;
   if (len > 0 && (!k || !v)) return fail(BDK_INVALID_ARGUMENT, "null k/v");
   const size_t n = (size_t)len * c->desc.head_dim;
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   void* d = nullptr;
   if (n) {
     BDK_CUDA(cudaMalloc(&d, 2 * n * 2), "cudaMalloc(prefill staging)");
@@ -1134,9 +1159,9 @@ bdk_status bdk_append_token_host(bdk_cache* c, uint32_t b, uint32_t h, const uin
   if (s) return s;
   if (!k || !v) return fail(BDK_INVALID_ARGUMENT, "null k/v row");
   const size_t d = c->desc.head_dim;
+  DevGuard dev_guard_(c->device);
   s = ensure_stage(c, 4 * d + 256);
   if (s) return s;
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
   uint16_t* dk = static_cast<uint16_t*>(c->d_stage);
   BDK_CUDA(cudaMemcpy(dk, k, d * 2, cudaMemcpyHostToDevice), "H2D row");
   BDK_CUDA(cudaMemcpy(dk + d, v, d * 2, cudaMemcpyHostToDevice), "H2D row");
@@ -1158,7 +1183,7 @@ bdk_status bdk_packed_tile_host(const bdk_cache* c, uint32_t b, uint32_t h, uint
   if (!k_out || !v_out) return fail(BDK_INVALID_ARGUMENT, "null output");
   const uint32_t blk0 = t0 / n_r, blk1 = (t0 + len + n_r - 1) / n_r, nb = blk1 - blk0;
   const size_t d = c->desc.head_dim, rows = (size_t)nb * n_r;
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   uint16_t* dbuf = nullptr;
   BDK_CUDA(cudaMalloc(&dbuf, 2 * rows * d * 2), "cudaMalloc(dequant)");
   s = bdk_dequant_blocks(c, b, h, blk0, nb, dbuf, dbuf + rows * d, nullptr);
@@ -1180,7 +1205,7 @@ static bdk_status read_record(const bdk_cache* c, int i, uint32_t blk, uint16_t*
                               uint16_t* vw, uint16_t* kp, uint16_t* vp) {
   const Geom& G = c->dev.G;
   std::vector<uint8_t> rec(G.rec_bytes);
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   BDK_CUDA(cudaDeviceSynchronize(), "sync");
   BDK_CUDA(cudaMemcpy(rec.data(),
                       c->dev.records + ((size_t)i * G.max_blocks + blk) * G.rec_bytes,
@@ -1215,7 +1240,7 @@ bdk_status bdk_build_block(bdk_cache* c, uint32_t b, uint32_t h, uint16_t* kw, u
     return fail(BDK_STATE_ERROR, "build_block requires a full residual (res_len == N_r)");
   if (c->packed_blocks[i] >= c->dev.G.max_blocks)
     return fail(BDK_CAPACITY_ERROR, "cache arena full (raise max_tokens)");
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   c->launches += 1;
   BDK_CUDA(bdk::launch_build(c->dev, i, nullptr), "build launch");
   c->blocks_written = true;  // the slot past the packed segment was written
@@ -1257,7 +1282,7 @@ bdk_status bdk_adopt_block(bdk_cache* c, uint32_t b, uint32_t h, const uint16_t*
   if (G.kp_bytes) std::memcpy(rec.data() + 2 * G.wbytes, kp, G.kp_bytes);
   if (G.vp_bytes) std::memcpy(rec.data() + 2 * G.wbytes + G.kp_bytes, vp, G.vp_bytes);
   const int slot = c->packed_blocks[i];
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   BDK_CUDA(cudaDeviceSynchronize(), "sync");
   BDK_CUDA(cudaMemcpy(c->dev.records + ((size_t)i * G.max_blocks + slot) * G.rec_bytes,
                       rec.data(), G.rec_bytes, cudaMemcpyHostToDevice),
@@ -1277,7 +1302,7 @@ bdk_status bdk_read_residual(const bdk_cache* c, uint32_t b, uint32_t h, uint16_
   const int i = cell_of(c, b, h);
   const size_t n = (size_t)c->res_len[i] * c->desc.head_dim;
   const size_t base = (size_t)i * c->dev.G.n_r * c->desc.head_dim;
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   BDK_CUDA(cudaDeviceSynchronize(), "sync");
   if (k && n) BDK_CUDA(cudaMemcpy(k, c->dev.res_k + base, n * 2, cudaMemcpyDeviceToHost), "D2H");
   if (v && n) BDK_CUDA(cudaMemcpy(v, c->dev.res_v + base, n * 2, cudaMemcpyDeviceToHost), "D2H");
@@ -1291,7 +1316,7 @@ bdk_status bdk_dequant_blocks(const bdk_cache* c, uint32_t b, uint32_t h, uint32
   const int i = cell_of(c, b, h);
   if (static_cast<int>(blk0 + nblk) > c->packed_blocks[i])
     return fail(BDK_SHAPE_ERROR, "packed_tile: range past packed segment");
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   c->launches += 1;
   BDK_CUDA(bdk::launch_dequant(c->dev, i, static_cast<int>(blk0), static_cast<int>(nblk),
                                static_cast<__half*>(k_out), static_cast<__half*>(v_out),
@@ -1320,7 +1345,7 @@ bdk_status bdk_corrupt_word(bdk_cache* c, uint32_t b, uint32_t h, uint32_t blk, 
   if (static_cast<int>(blk) >= c->packed_blocks[i] || word >= c->wpb)
     return fail(BDK_SHAPE_ERROR, "corrupt_word: index out of range");
   const Geom& G = c->dev.G;
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   BDK_CUDA(cudaDeviceSynchronize(), "sync");
   const_cast<bdk_cache*>(c)->blocks_written = true;
   BDK_CUDA(cudaMemcpy(c->dev.records + ((size_t)i * G.max_blocks + blk) * G.rec_bytes +
@@ -1340,7 +1365,7 @@ bdk_status bdk_profile_begin(bdk_cache* c) {
 bdk_status bdk_profile_end(bdk_cache* c, float* total_ms, uint32_t* launches) {
   if (!c || !total_ms || !launches) return fail(BDK_INVALID_ARGUMENT, "null argument");
   c->profiling = false;
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   float sum = 0.f;
   for (size_t i = 0; i < c->events_used; ++i) {
     BDK_CUDA(cudaEventSynchronize(c->events[i].second), "cudaEventSynchronize");
@@ -1427,7 +1452,7 @@ bdk_status serialize(const bdk_cache* c, std::vector<uint8_t>& o) {
   put_u32(o, d);
   put_u32(o, c->desc.batch);
   put_u32(o, c->desc.heads_kv);
-  BDK_CUDA(cudaSetDevice(c->device), "cudaSetDevice");
+  DevGuard dev_guard_(c->device);
   BDK_CUDA(cudaDeviceSynchronize(), "sync");
   std::vector<uint8_t> recs;
   std::vector<uint16_t> res;
@@ -1648,7 +1673,7 @@ struct DevBuf {  // scoped device allocation
 
 bdk_status quant_common(uint32_t bits, int32_t device) {
   if (bits == 0 || bits > 16) return fail(BDK_UNSUPPORTED_BITS, "num_bits must be 1..16");
-  BDK_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  DevGuard dev_guard_(device);
   return BDK_OK;
 }
 }  // namespace
@@ -1690,7 +1715,7 @@ bdk_status bdk_dequantize_tile(const uint16_t* codes, const uint16_t* params, ui
   const uint32_t extent = axis == 0 ? rows : d;
   if (group_size == 0 || extent % group_size != 0)
     return fail(BDK_SHAPE_ERROR, "dequantize_tile: group_size must divide the grouped extent");
-  BDK_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  DevGuard dev_guard_(device);
   const size_t n = (size_t)rows * d;
   const size_t groups = n / group_size;
   if (n == 0) return BDK_OK;
@@ -1743,7 +1768,7 @@ bdk_status bdk_quantize_group(const float* x, uint32_t n, float scale, float zer
 bdk_status bdk_dequantize_group(const uint16_t* codes, uint32_t n, float scale, float zero,
                                 float* values, int32_t device) {
   if (!codes || !values) return fail(BDK_INVALID_ARGUMENT, "null argument");
-  BDK_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  DevGuard dev_guard_(device);
   if (n == 0) return BDK_OK;
   DevBuf bc, bo;
   BDK_CUDA(cudaMalloc(&bc.p, (size_t)n * 2), "cudaMalloc");

@@ -140,8 +140,13 @@ struct SpanArgs {
   int keep_state = 0;  // parts already hold the initial state
   float* parts = nullptr;  // [cells][n_parts][rows * (d + 2)]
   int n_parts = 1;
+  // set by launch_span_parts: which stages fit in shared memory (else the K/V
+  // chunk is read from the source and the P.V sums live in `scratch`)
+  int kv_smem = 1, pacc_smem = 1;
+  float* scratch = nullptr;
 };
-// dynamic shared memory of one span CTA (tile = the longest tile it walks)
+// minimal dynamic shared memory of one span CTA (tile = the longest tile it
+// walks); the K/V chunk stage and P.V sums are added when they fit
 size_t span_smem_bytes(int rows, int d, int tile);
 cudaError_t launch_span_parts(const SpanArgs& a, int n_cells, cudaStream_t s);
 // combine (attention.cpp:142-162) of each cell's n_parts states -> out rows

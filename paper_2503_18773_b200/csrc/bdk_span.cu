@@ -60,7 +60,17 @@ __device__ __forceinline__ void stage_rows(const SpanCtx& x, int t0, int m, int 
   }
 }
 
-// online softmax over tokens [t_begin, t_end) in tiles of tile_n
+// K/V element j of the current chunk: the staged row, or (when the staged
+// layout does not fit in shared memory) straight from the source
+__device__ __forceinline__ float chunk_kv(const SpanCtx& x, const float* kv, int d, int t0, int j,
+                                          int c, int which) {
+  return kv ? kv[j * (d + 1) + c] : span_kv(x, t0 + j, c, which);
+}
+
+// online softmax over tokens [t_begin, t_end) in tiles of tile_n.  kv (the
+// chunk stage) may be null and pacc may live in global memory: the large
+// geometries the reference accepts (e.g. n_group 64, d 256, N_r 512) keep
+// only q, the score tile and the rescale factors in shared memory.
 __device__ void span_walk(const SpanCtx& x, const float* q, int rows, int d, float scale,
                           int tile_n, int t_begin, int t_end, float* o, float* m, float* l,
                           float* s, float* resc, float* pacc, float* kv) {
@@ -70,12 +80,13 @@ __device__ void span_walk(const SpanCtx& x, const float* q, int rows, int d, flo
     // S = scale * q k^T, sequential over channels
     for (int c0 = 0; c0 < n; c0 += kSpanChunk) {
       const int mc = min(kSpanChunk, n - c0);
-      stage_rows(x, t0 + c0, mc, d, 0, kv);
+      if (kv) stage_rows(x, t0 + c0, mc, d, 0, kv);
       __syncthreads();
       for (int i = tid; i < rows * mc; i += nt) {
         const int r = i / mc, j = i % mc;
         float acc = 0.f;
-        for (int c = 0; c < d; ++c) acc = __fadd_rn(acc, __fmul_rn(q[r * d + c], kv[j * (d + 1) + c]));
+        for (int c = 0; c < d; ++c)
+          acc = __fadd_rn(acc, __fmul_rn(q[r * d + c], chunk_kv(x, kv, d, t0 + c0, j, c, 0)));
         s[r * n + c0 + j] = __fmul_rn(acc, scale);
       }
       __syncthreads();
@@ -99,17 +110,18 @@ __device__ void span_walk(const SpanCtx& x, const float* q, int rows, int d, flo
     }
     for (int i = tid; i < rows * d; i += nt) pacc[i] = 0.f;
     // O' = P V + rescale * O, sequential over the tile's tokens (the running
-    // sum carries across chunks, so the order is the reference's)
+    // sum carries across chunks, so the order is the reference's; element i
+    // of pacc is owned by one thread throughout)
     for (int c0 = 0; c0 < n; c0 += kSpanChunk) {
       const int mc = min(kSpanChunk, n - c0);
       __syncthreads();
-      stage_rows(x, t0 + c0, mc, d, 1, kv);
+      if (kv) stage_rows(x, t0 + c0, mc, d, 1, kv);
       __syncthreads();
       for (int i = tid; i < rows * d; i += nt) {
         const int r = i / d, c = i % d;
         float acc = pacc[i];
         for (int j = 0; j < mc; ++j)
-          acc = __fadd_rn(acc, __fmul_rn(s[r * n + c0 + j], kv[j * (d + 1) + c]));
+          acc = __fadd_rn(acc, __fmul_rn(s[r * n + c0 + j], chunk_kv(x, kv, d, t0 + c0, j, c, 1)));
         pacc[i] = acc;
       }
     }
@@ -125,11 +137,14 @@ __global__ void __launch_bounds__(kSpanThreads) span_parts_kernel(SpanArgs a) {
   const int cell = a.cell0 + blockIdx.y, part = blockIdx.x;
   const Geom& G = a.c.G;
   const int tile_max = a.source == kSpanFp32 ? a.len32 : max(a.tile_n, G.n_r);
+  // shared layout: q | resc | s [rows * tile_max] | kv chunk (opt.) | pacc (opt.)
   float* q = sm;
   float* resc = q + rows * d;
-  float* pacc = resc + rows;
-  float* kv = pacc + rows * d;
-  float* s = kv + kSpanChunk * (d + 1);
+  float* s = resc + rows;
+  float* kv = a.kv_smem ? s + (size_t)rows * tile_max : nullptr;
+  float* pacc = a.pacc_smem
+                    ? s + (size_t)rows * tile_max + (a.kv_smem ? kSpanChunk * (d + 1) : 0)
+                    : a.scratch + ((size_t)blockIdx.y * a.n_parts + part) * rows * d;
   float* st = a.parts + ((size_t)blockIdx.y * a.n_parts + part) * rows * (d + 2);
   float* o = st;
   float* m = st + rows * d;
@@ -184,7 +199,6 @@ __global__ void __launch_bounds__(kSpanThreads) span_parts_kernel(SpanArgs a) {
     t_end = count ? min(lo + (first + count) * a.tile_n, hi) : t_begin;
   }
   __syncthreads();
-  (void)tile_max;
   span_walk(x, q, rows, d, a.scale, tile, t_begin, t_end, o, m, l, s, resc, pacc, kv);
 }
 
@@ -229,20 +243,45 @@ __global__ void partitioned_rowmax_kernel(const float* s, int rows, int cols, in
 
 }  // namespace
 
+// the minimal layout (q, rescale factors, score tile): what a geometry needs
+// to run at all
 size_t span_smem_bytes(int rows, int d, int tile) {
-  return ((size_t)rows * (2 * d + 1 + tile) + (size_t)kSpanChunk * (d + 1)) * sizeof(float);
+  return (size_t)rows * (d + 1 + tile) * sizeof(float);
 }
 
-cudaError_t launch_span_parts(const SpanArgs& a, int n_cells, cudaStream_t s) {
-  if (n_cells <= 0 || a.n_parts <= 0) return cudaSuccess;
+cudaError_t launch_span_parts(const SpanArgs& a_in, int n_cells, cudaStream_t s) {
+  if (n_cells <= 0 || a_in.n_parts <= 0) return cudaSuccess;
+  SpanArgs a = a_in;
   const int tile = a.source == kSpanFp32 ? a.len32 : max(a.tile_n, a.c.G.n_r);
-  const size_t smem = span_smem_bytes(a.rows, a.d, tile);
-  cudaError_t e = cudaFuncSetAttribute(span_parts_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  span_parts_kernel<<<dim3(a.n_parts, n_cells), kSpanThreads, smem, s>>>(a);
-  return cudaGetLastError();
+  // stage the K/V chunk and the running P.V sums in shared memory when they
+  // fit (227 KB per CTA); otherwise read K/V from the source and keep the
+  // sums in a stream-ordered global scratch
+  constexpr size_t kMax = 227u << 10;
+  const size_t kv_b = (size_t)kSpanChunk * (a.d + 1) * sizeof(float);
+  const size_t pacc_b = (size_t)a.rows * a.d * sizeof(float);
+  size_t smem = span_smem_bytes(a.rows, a.d, tile);
+  a.kv_smem = smem + kv_b <= kMax;
+  if (a.kv_smem) smem += kv_b;
+  a.pacc_smem = smem + pacc_b <= kMax;
+  if (a.pacc_smem) smem += pacc_b;
+  float* scratch = nullptr;
+  cudaError_t e;
+  if (!a.pacc_smem) {
+    e = cudaMallocAsync(&scratch, (size_t)n_cells * a.n_parts * pacc_b, s);
+    if (e != cudaSuccess) return e;
+    a.scratch = scratch;
+  }
+  e = cudaFuncSetAttribute(span_parts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+  if (e == cudaSuccess) {
+    span_parts_kernel<<<dim3(a.n_parts, n_cells), kSpanThreads, smem, s>>>(a);
+    e = cudaGetLastError();
+  }
+  if (scratch) {
+    const cudaError_t f = cudaFreeAsync(scratch, s);
+    if (e == cudaSuccess) e = f;
+  }
+  return e;
 }
 
 cudaError_t launch_span_combine(const float* parts, int n_cells, int n_parts, int rows, int d,

@@ -119,6 +119,13 @@ def _span_case(bits, axis, g, d, warp_n, hq, hkv, prefill, steps, tile_n, splits
     (4, 1, 32, 96, 1, 6, 3, 100, 40, 8, 5),      # KToken keys, head_dim 96
     (16, 0, 64, 64, 4, 4, 2, 180, 36, 32, 2),    # fp16 passthrough (test_attention.cpp:350)
     (4, 0, 128, 128, 4, 64, 4, 600, 10, 64, 4),  # head_dim 128 with n_group 16
+    # one requested split over ~300 tiles: decode_step raises the split count
+    # (no CTA walks more than 4 tiles) -- the result stays within 1e-5
+    (4, 0, 32, 64, 2, 4, 2, 5000, 3, 16, 1),
+    # n_group 64, d 256, N_r 512: the K/V chunk stage and P.V sums do not fit
+    # next to the score tile in shared memory, so the walk reads K/V from the
+    # records and keeps the sums in global scratch (same order)
+    (4, 0, 256, 256, 16, 64, 1, 600, 3, 128, 2),
 ])
 def test_span_decode_matches_oracle(bits, axis, g, d, warp_n, hq, hkv, prefill, steps, tile_n,
                                     splits):
