@@ -818,6 +818,58 @@ void orc_gauss_fill_rounded(orc_gauss* g, float* dst, size_t n) {
   for (size_t i = 0; i < n; ++i) dst[i] = orc_round_f16(orc_gauss_next(g));
 }
 
+/* The same stream as orc_gauss_fill_rounded, with the Box-Muller transforms
+ * (log/sqrt/sin/cos, the cost) spread over threads: the Mersenne Twister
+ * words are drawn sequentially, then pair k = (u1, u2) gives outputs 2k
+ * (r cos) and 2k+1 (r sin) independently.  Bit-identical to the sequential
+ * fill (tests/test_oracle.py). */
+typedef struct {
+  const uint64_t* raw;
+  float* dst;
+  size_t p0, p1;
+} gauss_job;
+
+static void* gauss_pairs(void* arg) {
+  const gauss_job* j = (const gauss_job*)arg;
+  for (size_t k = j->p0; k < j->p1; ++k) {
+    const double u1 = ((double)(j->raw[2 * k] >> 11) + 1.0) * 0x1.0p-53;
+    const double u2 = ((double)(j->raw[2 * k + 1] >> 11) + 1.0) * 0x1.0p-53;
+    const double r = sqrt(-2.0 * log(u1));
+    const double theta = 2.0 * 3.14159265358979323846 * u2;
+    j->dst[2 * k] = orc_round_f16((float)(r * cos(theta)));
+    j->dst[2 * k + 1] = orc_round_f16((float)(r * sin(theta)));
+  }
+  return NULL;
+}
+
+void orc_gauss_fill_rounded_par(orc_gauss* g, float* dst, size_t n, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 64) threads = 64;
+  size_t i = 0;
+  if (n && g->has_spare) dst[i++] = orc_round_f16(orc_gauss_next(g));
+  const size_t chunk_pairs = (size_t)1 << 22;
+  uint64_t* raw = (uint64_t*)malloc(2 * chunk_pairs * sizeof(uint64_t));
+  while (raw && n - i >= 2) {
+    const size_t pairs = (n - i) / 2 < chunk_pairs ? (n - i) / 2 : chunk_pairs;
+    for (size_t k = 0; k < 2 * pairs; ++k) raw[k] = mt_next(g);
+    pthread_t tid[64];
+    gauss_job job[64];
+    const int nt = pairs < 4096 ? 1 : threads;
+    for (int t = 0; t < nt; ++t) {
+      job[t].raw = raw;
+      job[t].dst = dst + i;
+      job[t].p0 = pairs * t / nt;
+      job[t].p1 = pairs * (t + 1) / nt;
+      if (t > 0) pthread_create(&tid[t], NULL, gauss_pairs, &job[t]);
+    }
+    gauss_pairs(&job[0]);
+    for (int t = 1; t < nt; ++t) pthread_join(tid[t], NULL);
+    i += 2 * pairs;
+  }
+  free(raw);
+  for (; i < n; ++i) dst[i] = orc_round_f16(orc_gauss_next(g));
+}
+
 void orc_gauss_fill_f16(orc_gauss* g, uint16_t* dst, size_t n) {
   for (size_t i = 0; i < n; ++i) dst[i] = orc_f32_to_f16_bits(orc_gauss_next(g));
 }

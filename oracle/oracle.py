@@ -119,6 +119,7 @@ class Oracle:
             L.orc_gauss_next.argtypes = [C.c_void_p]
             L.orc_gauss_fill_rounded.argtypes = [C.c_void_p, _f32p, _sz]
             L.orc_gauss_fill_f16.argtypes = [C.c_void_p, _u16p, _sz]
+            L.orc_gauss_fill_rounded_par.argtypes = [C.c_void_p, _f32p, _sz, C.c_int]
             L.orc_fnv1a64.restype = C.c_uint64
             L.orc_fnv1a64.argtypes = [C.c_void_p, _sz, C.c_uint64]
             cls._lib = L
@@ -237,9 +238,14 @@ class Gauss:
     def next(self) -> float:
         return lib().orc_gauss_next(self._buf)
 
-    def rounded(self, n: int) -> np.ndarray:
+    def rounded(self, n: int, threads: int = 1) -> np.ndarray:
+        """n fp16-rounded draws; threads > 1 spreads the Box-Muller
+        transforms over host threads (the same stream, bit for bit)."""
         out = np.empty(n, np.float32)
-        lib().orc_gauss_fill_rounded(self._buf, out, n)
+        if threads > 1:
+            lib().orc_gauss_fill_rounded_par(self._buf, out, n, threads)
+        else:
+            lib().orc_gauss_fill_rounded(self._buf, out, n)
         return out
 
     def f16(self, n: int) -> np.ndarray:

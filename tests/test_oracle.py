@@ -241,3 +241,16 @@ def test_oracle_blocks_equal_live_reference_on_adversarial_data(bits, wn):
         for i in range(rc.packed_len(0, h) // rc.n_r):
             for x, y in zip(rc.block(0, h, i), oc.block(0, h, i)):
                 assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("n,skip", [(0, 0), (1, 1), (7, 0), (4097, 1), (2_000_003, 0)])
+def test_parallel_gauss_fill_is_the_same_stream(n, skip):
+    """bench.py draws the run_bench stream (bench.cpp:18-35) with the
+    Box-Muller transforms spread over threads: bit-identical to the
+    sequential fill, including a pending spare and an odd length."""
+    a, b = O.Gauss(11), O.Gauss(11)
+    for _ in range(skip):
+        a.next(), b.next()
+    x, y = a.rounded(n), b.rounded(n, threads=6)
+    assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    assert a.next() == b.next()
