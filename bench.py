@@ -800,7 +800,7 @@ def parity_qpack(name, local, threads=None):
     for cell in fx["cells"]:
         b, h = cell["b"], cell["h"]
         hs = hashlib.sha256()
-        for i in range(c.packed_len(b, h) // c.n_r):
+        for i in range(c.packed_len(b, h) // c.n_r()):
             blk = c.block(b, h, i)
             for a in (blk.k_words, blk.v_words, blk.k_params, blk.v_params):
                 hs.update(np.ascontiguousarray(a).astype("<u2").tobytes())

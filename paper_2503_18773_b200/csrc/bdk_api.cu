@@ -302,7 +302,8 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
   // PDL: overlap this launch's prologue (and, unless the previous step wrote
   // a block, its first TMA prefetches) with the tail of the previous kernel
   a.pdl = pdl_off || a.ev_begin ? 0 : 1;
-  a.prefetch_ok = c->blocks_written ? 0 : 1;
+  static const bool prefetch_off = getenv("BDK_PREFETCH") && atoi(getenv("BDK_PREFETCH")) == 0;
+  a.prefetch_ok = (c->blocks_written || prefetch_off) ? 0 : 1;
   c->blocks_written = false;
   unsigned long long* trace = nullptr;
   if (trace_path) {

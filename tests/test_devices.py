@@ -77,4 +77,4 @@ def test_device_outputs_are_validated():
         bk.decode_step(c, cfg, q.cpu().float().numpy(), kn.cpu().float().numpy(),
                        kn.cpu().float().numpy(), out=np.empty((1, 8, D), np.float64))
     # nothing was appended by the rejected calls
-    assert c.res_len(0, 0) == 300 % c.n_r
+    assert c.res_len(0, 0) == 300 % c.n_r()

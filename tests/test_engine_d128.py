@@ -58,7 +58,7 @@ def _worst(cache, q, out, k_hist, v_hist, hq, hkv, quantized, bits=16, g=64):
         for h in range(hkv):
             kc, vc = k_hist[b, h], v_hist[b, h]
             if quantized:
-                kc, vc = O.offline_quant_reference(kc, vc, bits, 0, g, cache.n_r)
+                kc, vc = O.offline_quant_reference(kc, vc, bits, 0, g, cache.n_r())
             for r in range(ng):
                 qh = h * ng + r
                 ref = O.naive_attention(q[b, qh], kc, vc)[0]
@@ -86,11 +86,14 @@ def test_passthrough_decode_matches_naive_oracle_d128():
     assert worst < TOL
 
 
-@pytest.mark.parametrize("bits,g", [(2, 128), (4, 128), (8, 128), (2, 32), (4, 32), (8, 32)])
-def test_quantized_decode_equals_naive_on_dequantized_kv_d128(bits, g):
-    # test_attention.cpp:370-399 at d = 128 (group 128 is the BASELINE group;
-    # group 32 keeps the reference's small-group case)
-    cache, q, out, kh, vh = _engine_case(1, 2, 1, bits, g, 2, 700, 3, seed=1000 + bits, tile_n=16)
+@pytest.mark.parametrize("bits,g,warp_n", [(2, 128, 2), (4, 128, 4), (8, 128, 8), (2, 32, 2),
+                                           (4, 32, 2), (8, 32, 2)])
+def test_quantized_decode_equals_naive_on_dequantized_kv_d128(bits, g, warp_n):
+    # test_attention.cpp:370-399 at d = 128 (group 128 is the BASELINE group,
+    # warp_n chosen so that it divides N_r; group 32 keeps the reference's
+    # small-group case)
+    cache, q, out, kh, vh = _engine_case(1, 2, 1, bits, g, warp_n, 700, 3, seed=1000 + bits,
+                                         tile_n=8 * warp_n)
     worst = _worst(cache, q, out, kh, vh, 2, 1, True, bits, g)
     print(f"{bits}-bit g{g} d128: max-abs {worst:.2e}")
     assert worst < TOL
@@ -119,7 +122,7 @@ def test_nth_step_flushes_exactly_once_d128():
     from paper_2503_18773_b200 import bitkv as bk
     spec = bk.QuantSpec(8, bk.QuantAxis.KChannel, 32)
     cache = bk.KVCache(1, 1, D, 2, spec, max_tokens=256)
-    n_r = cache.n_r
+    n_r = cache.n_r()
     cfg = bk.AttentionConfig(batch=1, heads_q=1, heads_kv=1, head_dim=D, tile_m=1, tile_n=16,
                              num_splits=1, warp_n=2)
     g = O.Gauss(55)

@@ -8,7 +8,7 @@ python -c "from paper_2503_18773_b200 import build as B; assert not B._stale(), 
 nvidia-smi -q -d CLOCK,PERFORMANCE > $O/smi_before.txt 2>&1
 timeout 1500 python -m pytest ${TESTS:-tests} -m gpu -x -q -rA > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 if [ -z "$NOBENCH" ]; then
-  /usr/bin/time -v timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err
+  timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err
   echo "bench rc=$?" >> $O/bench.err
 fi
 echo done

@@ -1,14 +1,14 @@
 #!/bin/bash
 # Knob sweep (dev): bench lines per (env setting, workload).  KNOBS is a list
 # of "ENV=VAL" strings ("-" = defaults), WL a list of workloads.
-mkdir -p gpurun_out/knobs
-O=gpurun_out/knobs
+mkdir -p gpurun_out/${KOUT:-knobs}
+O=gpurun_out/${KOUT:-knobs}
 python -c "from paper_2503_18773_b200 import build as B; assert not B._stale(), \"stale lib\"" || exit 3
 if [ -n "$TESTS" ]; then timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log; fi
 for k in ${KNOBS:--}; do for w in ${WL:-C2 C5}; do
   tag=$(echo "$k" | tr '=/' '__')
   if [ "$k" = "-" ]; then envs=""; else envs="$k"; fi
-  env $envs timeout 300 python bench.py --workload $w --no-cpu-baseline --e2e-steps ${E2E:-20} --soak 0.3 > $O/b_${w}_${tag}.json 2> $O/b_${w}_${tag}.err
+  env $envs timeout 300 python bench.py --workload $w --quick --no-cpu-baseline --e2e-steps ${E2E:-20} --soak 0.3 > $O/b_${w}_${tag}.json 2> $O/b_${w}_${tag}.err
   python - "$O/b_${w}_${tag}.json" "$k" "$w" >> $O/summary.txt <<'PY'
 import json, sys
 try:
