@@ -149,6 +149,26 @@ BDK_API bdk_status bdk_flush_residual(bdk_cache* cache, uint32_t b, uint32_t h, 
 BDK_API bdk_status bdk_decode_step(bdk_cache* cache, const bdk_attn_config* cfg,
                                    const void* q_dev, const void* k_new_dev,
                                    const void* v_new_dev, float* out_dev, void* stream);
+/* A CUDA graph of n_steps consecutive decode steps (decode_step,
+ * attention.cpp:164-242, Algorithm 2's steady-state loop): step i reads
+ * q_dev + i*batch*heads_q*d, k_new_dev/v_new_dev + i*batch*heads_kv*d
+ * (binary16) and writes out_dev + i*batch*heads_q*d (fp32).  Every step is
+ * ONE launch -- append, attention, combine and the flush of a residual
+ * window that fills (build_block + commit_block, kvcache.cpp:208-237) --
+ * scheduled on the device from the cache's device lengths, so one captured
+ * graph replays correctly at any cache state, flush steps included, and
+ * bit-identically to the same steps run eagerly.  Fast mode only
+ * (bdk_set_precise(cache, 0); else BDK_UNSUPPORTED).  Each launch checks the
+ * host mirror's capacity for n_steps more tokens first (CapacityError) and
+ * advances it.  The graph keeps pointers to the cache's workspaces: destroy
+ * it before the cache. */
+typedef struct bdk_graph bdk_graph;
+BDK_API bdk_status bdk_graph_create(bdk_cache* cache, const bdk_attn_config* cfg,
+                                    const void* q_dev, const void* k_new_dev,
+                                    const void* v_new_dev, float* out_dev, uint32_t n_steps,
+                                    bdk_graph** graph);
+BDK_API bdk_status bdk_graph_launch(bdk_graph* graph, void* stream);
+BDK_API bdk_status bdk_graph_destroy(bdk_graph* graph);
 /* Same contract with host fp32 tensors (the reference's by-value Tensor /
  * AttnOutput interface); synchronous; host<->device copies included. */
 BDK_API bdk_status bdk_decode_step_host(bdk_cache* cache, const bdk_attn_config* cfg,

@@ -65,6 +65,10 @@ SIGNATURES = {
     "bdk_flush_residual": (C.c_int, [vp, u32, u32, vp]),
     "bdk_decode_step": (C.c_int, [vp, C.POINTER(AttnConfig), vp, vp, vp, vp, vp]),
     "bdk_decode_step_host": (C.c_int, [vp, C.POINTER(AttnConfig), vp, vp, vp, vp]),
+    "bdk_graph_create": (C.c_int, [vp, C.POINTER(AttnConfig), vp, vp, vp, vp, u32,
+                                   C.POINTER(vp)]),
+    "bdk_graph_launch": (C.c_int, [vp, vp]),
+    "bdk_graph_destroy": (C.c_int, [vp]),
     "bdk_decode_partial": (C.c_int, [vp, C.POINTER(AttnConfig), vp, vp, vp, u32, u32, u32, vp,
                                      vp, vp]),
     "bdk_merge_partials": (C.c_int, [vp, vp, u32, u32, u32, C.c_uint64, C.c_uint64, vp, vp]),

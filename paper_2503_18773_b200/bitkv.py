@@ -782,6 +782,52 @@ class DecodeStepper:
             _check(st)
 
 
+class DecodeGraph:
+    """A CUDA graph of ``n`` consecutive decode steps (bdk_graph_create): the
+    steady-state loop of Algorithm 2 -- append, attention, combine and the
+    flush of any residual that fills, one kernel per step -- captured once
+    and replayed at any cache state.  ``qs`` [n, batch, heads_q, d],
+    ``ks``/``vs`` [n, batch, heads_kv, d] (contiguous CUDA fp16, refill them
+    in place between launches) and ``outs`` [n, batch, heads_q, d] (fp32).
+    Fast mode only.  Replays are bit-identical to the same steps run with
+    :func:`decode_step`."""
+
+    def __init__(self, cache: KVCache, cfg: AttentionConfig, qs, ks, vs, outs):
+        n = qs.shape[0]
+        shape_q = (n, cfg.batch, cfg.heads_q, cfg.head_dim)
+        shape_kv = (n, cfg.batch, cfg.heads_kv, cfg.head_dim)
+        for t, shp in ((qs, shape_q), (ks, shape_kv), (vs, shape_kv)):
+            if not (t.is_cuda and t.dtype == torch.float16 and t.is_contiguous()
+                    and tuple(t.shape) == shp and t.device.index == cache._device):
+                raise ShapeError(f"DecodeGraph inputs must be contiguous CUDA fp16 {shp}")
+        _check_f32_out(outs, shape_q, cache, "outs")
+        self._cfg = cfg._c()
+        h = C.c_void_p()
+        _check(_L.load().bdk_graph_create(cache.handle(), C.byref(self._cfg),
+                                          C.c_void_p(qs.data_ptr()), C.c_void_p(ks.data_ptr()),
+                                          C.c_void_p(vs.data_ptr()), C.c_void_p(outs.data_ptr()),
+                                          n, C.byref(h)))
+        self._h = h
+        self.n_steps = n
+        self._keep = (cache, qs, ks, vs, outs)
+
+    def launch(self, stream=None) -> None:
+        """Run the n steps (stream-ordered, no sync)."""
+        _check(_L.load().bdk_graph_launch(self._h, stream if stream is not None
+                                          else _stream_ptr()))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _L.load().bdk_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def decode_partial(cache: KVCache, cfg: AttentionConfig, q, k_new=None, v_new=None,
                    blk_begin: int = 0, blk_end: int = 1 << 30, out=None, lse=None,
                    include_residual: bool = True):

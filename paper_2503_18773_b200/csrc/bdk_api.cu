@@ -45,16 +45,16 @@ struct bdk_cache {
   void* d_stage = nullptr;
   size_t stage_bytes = 0;
   // fast-path (stream-K) resources
-  int* unit_off = nullptr;            // device [cells + 1]
-  std::vector<int> unit_off_host;     // last uploaded schedule
+  uint64_t fast_steps = 0;            // fast decode launches (= the device step counter)
+  bool capturing_pdl_off = false;     // graph capture without programmatic launch edges
   int* counters = nullptr;            // device [cells]
+  int graphs = 0;                     // live bdk_graph objects (workspaces are pinned)
   float* slots = nullptr;             // device partial slots
   size_t slot_floats = 0;
   int fast_ctas_per_sm = -1, fast_ng = -1;
   // attention-kernel timing (bdk_profile_begin/end): one event pair per launch
   bool profiling = false;
   mutable uint64_t launches = 0;  // kernels this cache has launched (all entry points)
-  bool blocks_written = true;  // a packed record may have changed since the last decode
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
   size_t events_used = 0;
 };
@@ -219,9 +219,37 @@ bdk_status next_events(bdk_cache* c, cudaEvent_t* e0, cudaEvent_t* e1) {
   return BDK_OK;
 }
 
-// Stream-K fast path (bdk_decode_fast.cu): schedule from the host mirror of
-// the lengths, one launch for append + attention + combine, then the flush of
-// any residual the step filled.
+// The live half of the double-buffered device lengths (DevCache::len2) for
+// kernels that update lengths in place (prefill, append, flush, precise and
+// span decode, readback): half (fast steps & 1).
+void point_lengths(bdk_cache* c) {
+  const size_t cells = (size_t)c->desc.batch * c->desc.heads_kv;
+  const size_t par = c->fast_steps & 1;
+  c->dev.packed_blocks = c->dev.len2 + par * 2 * cells;
+  c->dev.res_len = c->dev.packed_blocks + cells;
+}
+
+// mirror of one fast step's commit: every cell +1 token when it appends, a
+// full window becomes a block; the device step counter moved to the other half
+void advance_fast_step(bdk_cache* c, bool appends) {
+  if (appends) {
+    for (size_t i = 0; i < c->res_len.size(); ++i) {
+      if (++c->res_len[i] == c->dev.G.n_r) {
+        c->res_len[i] = 0;
+        c->packed_blocks[i] += 1;
+      }
+    }
+  }
+  c->fast_steps += 1;
+  point_lengths(c);
+}
+
+// Stream-K fast path (bdk_decode_fast.cu): ONE launch per step -- append,
+// attention, combine and the flush of any residual the step fills -- with the
+// schedule derived on the device from the double-buffered lengths, so the
+// launch arguments never change from step to step (a captured CUDA graph of
+// steps replays correctly).  The host mirror follows the same length
+// arithmetic for the reference's precondition checks.
 bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void* q,
                            const void* k_new, const void* v_new, float* out, float* lse,
                            int blk_begin, int blk_end, cudaStream_t stream, bool no_res) {
@@ -235,34 +263,19 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
     if (c->fast_ctas_per_sm <= 0)
       return fail(BDK_CUDA_ERROR, "fast decode kernel does not fit on this device");
   }
-  // schedule: [unit_off (cells + 1) | unit_nb (cells)]; a cell's units are its
-  // packed blocks in range then ceil(res_len' / (16 * warp_n)) residual units
-  const int rt = bdk::fast_residual_tokens(G);
-  std::vector<int> off(2 * cells + 1, 0);
-  for (int i = 0; i < cells; ++i) {
-    const int nb = std::max(0, std::min(blk_end, c->packed_blocks[i]) - blk_begin);
-    const int rlen = no_res ? 0 : c->res_len[i] + (k_new != nullptr ? 1 : 0);
-    const int nres = std::max(1, (rlen + rt - 1) / rt);
-    off[i + 1] = off[i] + nb + nres;
-    off[cells + 1 + i] = nb;
-  }
-  if (!c->unit_off) {
-    BDK_CUDA(cudaMalloc(&c->unit_off, (2 * cells + 1) * sizeof(int)), "cudaMalloc(schedule)");
+  const int n_ctas = c->fast_ctas_per_sm * c->num_sms;  // one wave, every step
+  if (!c->counters) {
     BDK_CUDA(cudaMalloc(&c->counters, cells * sizeof(int)), "cudaMalloc(counters)");
-    BDK_CUDA(cudaMemset(c->counters, 0, cells * sizeof(int)), "cudaMemset(counters)");
+    BDK_CUDA(cudaMemsetAsync(c->counters, 0, cells * sizeof(int), stream), "cudaMemset(counters)");
   }
-  if (off != c->unit_off_host) {
-    BDK_CUDA(cudaMemcpyAsync(c->unit_off, off.data(), (2 * cells + 1) * sizeof(int),
-                             cudaMemcpyHostToDevice, stream),
-             "H2D schedule");
-    c->unit_off_host = off;
-  }
-  const long long T = off[cells];
-  const int n_ctas =
-      static_cast<int>(std::min<long long>(T, (long long)c->fast_ctas_per_sm * c->num_sms));
   const size_t need = (size_t)(n_ctas + cells) * bdk::slot_stride(ng);
   if (need > c->slot_floats) {
-    if (c->slots) cudaFree(c->slots);
+    if (c->graphs > 0)
+      return fail(BDK_STATE_ERROR, "decode workspace would move under a live bdk_graph");
+    if (c->slots) {
+      BDK_CUDA(cudaStreamSynchronize(stream), "slots resize");
+      cudaFree(c->slots);
+    }
     c->slots = nullptr;
     BDK_CUDA(cudaMalloc(&c->slots, need * sizeof(float)), "cudaMalloc(slots)");
     c->slot_floats = need;
@@ -275,20 +288,11 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
   a.out_lse = lse;
   a.slots = c->slots;
   a.counters = c->counters;
-  a.unit_off = c->unit_off;
-  a.unit_nb = c->unit_off + cells + 1;
-  a.total_units = T;
-  {
-    bool uni = true;
-    for (int i = 1; i < cells && uni; ++i)
-      uni = off[i + 1] - off[i] == off[1] - off[0] && off[cells + 1 + i] == off[cells + 1];
-    a.uni_units = uni ? off[1] - off[0] : 0;
-    a.uni_nb = uni ? off[cells + 1] : 0;
-  }
   a.n_ctas = n_ctas;
   a.heads_q = static_cast<int>(cfg->heads_q);
   a.n_group = ng;
   a.blk_begin = blk_begin;
+  a.blk_end = blk_end;
   a.skip_residual = no_res ? 1 : 0;
   a.sm_scale_log2 = (1.0f / std::sqrt(static_cast<float>(cfg->head_dim))) * bdk::kLog2e;
   bdk_status st = next_events(c, &a.ev_begin, &a.ev_end);
@@ -299,12 +303,8 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
   static const int dev_flags = getenv("BDK_DEV_FLAGS") ? atoi(getenv("BDK_DEV_FLAGS")) : 0;
   static const bool pdl_off = getenv("BDK_PDL") && atoi(getenv("BDK_PDL")) == 0;
   a.dev_flags = dev_flags;
-  // PDL: overlap this launch's prologue (and, unless the previous step wrote
-  // a block, its first TMA prefetches) with the tail of the previous kernel
-  a.pdl = pdl_off || a.ev_begin ? 0 : 1;
-  static const bool prefetch_off = getenv("BDK_PREFETCH") && atoi(getenv("BDK_PREFETCH")) == 0;
-  a.prefetch_ok = (c->blocks_written || prefetch_off) ? 0 : 1;
-  c->blocks_written = false;
+  // PDL: overlap this launch's prologue with the tail of the previous kernel
+  a.pdl = pdl_off || a.ev_begin || c->capturing_pdl_off ? 0 : 1;
   unsigned long long* trace = nullptr;
   if (trace_path) {
     BDK_CUDA(cudaMalloc(&trace, (size_t)n_ctas * 16 * 8), "cudaMalloc(trace)");
@@ -320,7 +320,7 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
     BDK_CUDA(cudaStreamSynchronize(stream), "trace sync");
     cudaFree(trace);
     if (FILE* f = fopen(trace_path, "a")) {
-      fprintf(f, "launch n_ctas=%d T=%lld\n", n_ctas, T);
+      fprintf(f, "launch n_ctas=%d\n", n_ctas);
       for (int i = 0; i < n_ctas; ++i) {
         for (int k = 0; k < 16; ++k) fprintf(f, "%llu ", h[(size_t)i * 16 + k]);
         fprintf(f, "\n");
@@ -328,21 +328,9 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
       fclose(f);
     }
   }
-  if (k_new != nullptr) {
-    bool any_full = false;
-    for (int i = 0; i < cells; ++i) any_full |= (c->res_len[i] + 1 == G.n_r);
-    if (any_full) {
-      BDK_CUDA(bdk::launch_flush_full(c->dev, stream), "flush launch");
-      c->launches += 1;
-      c->blocks_written = true;
-    }
-    for (int i = 0; i < cells; ++i) {
-      if (++c->res_len[i] == G.n_r) {
-        c->res_len[i] = 0;
-        c->packed_blocks[i] += 1;
-      }
-    }
-  }
+  // the step's length commit, mirrored: the device lengths now live in the
+  // other half of the double buffer
+  advance_fast_step(c, k_new != nullptr && !no_res);
   return BDK_OK;
 }
 
@@ -412,7 +400,6 @@ bdk_status run_decode_span(bdk_cache* c, const bdk_attn_config* cfg, const void*
     if (full) {
       BDK_CUDA(bdk::launch_flush_full(c->dev, stream), "flush launch");
       c->launches += 1;
-      c->blocks_written = true;
     }
     for (int i = 0; i < cells; ++i) {
       if (++c->res_len[i] == c->dev.G.n_r) {
@@ -576,10 +563,11 @@ bdk_status bdk_cache_create(const bdk_cache_desc* d, bdk_cache** out) {
     e = cudaMalloc(&c->dev.records, cells * G.max_blocks * (size_t)G.rec_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->dev.res_k, cells * n_r * d->head_dim * 2);
   if (e == cudaSuccess) e = cudaMalloc(&c->dev.res_v, cells * n_r * d->head_dim * 2);
-  if (e == cudaSuccess) e = cudaMalloc(&c->dev.packed_blocks, cells * sizeof(int));
-  if (e == cudaSuccess) e = cudaMalloc(&c->dev.res_len, cells * sizeof(int));
-  if (e == cudaSuccess) e = cudaMemset(c->dev.packed_blocks, 0, cells * sizeof(int));
-  if (e == cudaSuccess) e = cudaMemset(c->dev.res_len, 0, cells * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->dev.len2, 4 * cells * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->dev.sched, 16 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->dev.len2, 0, 4 * cells * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->dev.sched, 0, 16 * sizeof(int));
+  point_lengths(c);
   if (e != cudaSuccess) {
     bdk_cache_destroy(c);
     return cuda_fail(e, "bdk_cache_create");
@@ -594,12 +582,11 @@ bdk_status bdk_cache_destroy(bdk_cache* c) {
   cudaFree(c->dev.records);
   cudaFree(c->dev.res_k);
   cudaFree(c->dev.res_v);
-  cudaFree(c->dev.packed_blocks);
-  cudaFree(c->dev.res_len);
+  cudaFree(c->dev.len2);
+  cudaFree(c->dev.sched);
   cudaFree(c->part_o);
   cudaFree(c->part_ml);
   cudaFree(c->span_parts);
-  cudaFree(c->unit_off);
   cudaFree(c->counters);
   cudaFree(c->slots);
   for (auto& ev : c->events) {
@@ -647,7 +634,6 @@ bdk_status bdk_prefill(bdk_cache* c, uint32_t b, uint32_t h, const void* k, cons
   if (len > 0 && (!k || !v)) return fail(BDK_INVALID_ARGUMENT, "null k/v");
   DevGuard dev_guard_(c->device);
   c->launches += 1;
-  c->blocks_written = true;
   BDK_CUDA(bdk::launch_prefill(c->dev, static_cast<const __half*>(k),
                                static_cast<const __half*>(v), static_cast<int>(len), i, 1,
                                as_stream(stream)),
@@ -667,7 +653,6 @@ bdk_status bdk_cache_reset(bdk_cache* c, void* stream) {
            "reset res_len");
   std::fill(c->packed_blocks.begin(), c->packed_blocks.end(), 0);
   std::fill(c->res_len.begin(), c->res_len.end(), 0);
-  c->blocks_written = true;
   return BDK_OK;
 }
 
@@ -682,7 +667,6 @@ bdk_status bdk_prefill_all(bdk_cache* c, const void* k, const void* v, uint32_t 
   const int cells = static_cast<int>(c->res_len.size());
   DevGuard dev_guard_(c->device);
   c->launches += 1;
-  c->blocks_written = true;
   BDK_CUDA(bdk::launch_prefill(c->dev, static_cast<const __half*>(k),
                                static_cast<const __half*>(v), static_cast<int>(len), 0, cells,
                                as_stream(stream)),
@@ -722,7 +706,6 @@ bdk_status bdk_flush_residual(bdk_cache* c, uint32_t b, uint32_t h, void* stream
   DevGuard dev_guard_(c->device);
   c->launches += 1;
   BDK_CUDA(bdk::launch_flush(c->dev, i, as_stream(stream)), "flush launch");
-  c->blocks_written = true;
   c->packed_blocks[i] += 1;
   c->res_len[i] = 0;
   return BDK_OK;
@@ -751,6 +734,113 @@ bdk_status bdk_decode_partial(bdk_cache* c, const bdk_attn_config* cfg, const vo
   return run_decode(c, cfg, q, k_new, v_new, out, lse, static_cast<int>(blk_begin),
                     static_cast<int>(std::min<uint32_t>(blk_end, 1u << 30)), as_stream(stream),
                     no_res);
+}
+
+struct bdk_graph {
+  bdk_cache* cache = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint32_t n_steps = 0;
+};
+
+bdk_status bdk_graph_create(bdk_cache* c, const bdk_attn_config* cfg, const void* q,
+                            const void* k_new, const void* v_new, float* out, uint32_t n_steps,
+                            bdk_graph** graph) {
+  if (!graph) return fail(BDK_INVALID_ARGUMENT, "null graph");
+  *graph = nullptr;
+  bdk_status s = check_decode(c, cfg, true);
+  if (s) return s;
+  if (!q || !k_new || !v_new || !out) return fail(BDK_INVALID_ARGUMENT, "null tensor");
+  if (n_steps == 0) return fail(BDK_INVALID_ARGUMENT, "n_steps must be > 0");
+  if (c->profiling) return fail(BDK_STATE_ERROR, "graph capture while profiling");
+  const int ng = static_cast<int>(cfg->heads_q / cfg->heads_kv);
+  if (c->precise || !exact_ok(c, cfg) || !bdk::fast_decode_ok(c->dev.G, ng))
+    return fail(BDK_UNSUPPORTED, "graph capture needs the fast decode path (set_precise(0))");
+  DevGuard dev_guard_(c->device);
+  cudaStream_t st = nullptr;
+  BDK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+  // the workspaces a step uses exist before capture (allocations do not
+  // belong in a graph): one attend-only launch sizes them
+  const auto pb0 = c->packed_blocks, rl0 = c->res_len;
+  const uint64_t steps0 = c->fast_steps, launches0 = c->launches;
+  s = run_decode_fast(c, cfg, q, nullptr, nullptr, out, nullptr, 0, 1 << 30, st, false);
+  if (s == BDK_OK && cudaStreamSynchronize(st) != cudaSuccess)
+    s = cuda_fail(cudaGetLastError(), "graph warm-up");
+  // capture: the host mirror advances as the steps are recorded (capacity
+  // checks run per step) and is restored afterwards -- the steps happen when
+  // the graph is launched
+  const size_t nq = (size_t)cfg->batch * cfg->heads_q * cfg->head_dim;
+  const size_t nk = (size_t)cfg->batch * cfg->heads_kv * cfg->head_dim;
+  cudaGraph_t g = nullptr;
+  if (s == BDK_OK) {
+    cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) s = cuda_fail(e, "cudaStreamBeginCapture");
+    for (uint32_t i = 0; s == BDK_OK && i < n_steps; ++i) {
+      s = check_decode(c, cfg, true);
+      if (s == BDK_OK)
+        s = run_decode_fast(c, cfg, static_cast<const __half*>(q) + i * nq,
+                            static_cast<const __half*>(k_new) + i * nk,
+                            static_cast<const __half*>(v_new) + i * nk, out + i * nq, nullptr, 0,
+                            1 << 30, st, false);
+    }
+    if (e == cudaSuccess) {
+      const cudaError_t e2 = cudaStreamEndCapture(st, &g);
+      if (s == BDK_OK && e2 != cudaSuccess) s = cuda_fail(e2, "cudaStreamEndCapture");
+    }
+  }
+  c->packed_blocks = pb0;
+  c->res_len = rl0;
+  c->fast_steps = steps0 + (s == BDK_OK ? 1 : 0);  // the warm-up was a real (attend-only) step
+  c->launches = launches0 + (s == BDK_OK ? 1 : 0);
+  point_lengths(c);
+  cudaGraphExec_t exec = nullptr;
+  if (s == BDK_OK) {
+    const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+    if (e != cudaSuccess) s = cuda_fail(e, "cudaGraphInstantiate");
+  }
+  if (g) cudaGraphDestroy(g);
+  cudaStreamDestroy(st);
+  if (s) return s;
+  auto* gr = new bdk_graph;
+  gr->cache = c;
+  gr->exec = exec;
+  gr->n_steps = n_steps;
+  c->graphs += 1;
+  *graph = gr;
+  return BDK_OK;
+}
+
+bdk_status bdk_graph_launch(bdk_graph* gr, void* stream) {
+  if (!gr || !gr->exec) return fail(BDK_INVALID_ARGUMENT, "null graph");
+  bdk_cache* c = gr->cache;
+  // capacity of the n_steps appends, on a copy of the mirror
+  {
+    auto pb = c->packed_blocks;
+    auto rl = c->res_len;
+    const int n_r = c->dev.G.n_r;
+    for (uint32_t i = 0; i < gr->n_steps; ++i)
+      for (size_t k = 0; k < rl.size(); ++k) {
+        if (rl[k] + 1 == n_r && pb[k] >= c->dev.G.max_blocks)
+          return fail(BDK_CAPACITY_ERROR, "cache arena full (raise max_tokens)");
+        if (++rl[k] == n_r) {
+          rl[k] = 0;
+          pb[k] += 1;
+        }
+      }
+  }
+  DevGuard dev_guard_(c->device);
+  BDK_CUDA(cudaGraphLaunch(gr->exec, as_stream(stream)), "cudaGraphLaunch");
+  for (uint32_t i = 0; i < gr->n_steps; ++i) advance_fast_step(c, true);
+  c->launches += gr->n_steps;
+  return BDK_OK;
+}
+
+bdk_status bdk_graph_destroy(bdk_graph* gr) {
+  if (!gr) return BDK_OK;
+  DevGuard dev_guard_(gr->cache->device);
+  if (gr->exec) cudaGraphExecDestroy(gr->exec);
+  gr->cache->graphs -= 1;
+  delete gr;
+  return BDK_OK;
 }
 
 bdk_status bdk_merge_partials(const float* o, const float* lse, uint32_t n_parts, uint32_t rows,
@@ -1244,7 +1334,6 @@ bdk_status bdk_build_block(bdk_cache* c, uint32_t b, uint32_t h, uint16_t* kw, u
   DevGuard dev_guard_(c->device);
   c->launches += 1;
   BDK_CUDA(bdk::launch_build(c->dev, i, nullptr), "build launch");
-  c->blocks_written = true;  // the slot past the packed segment was written
   return read_record(c, i, (uint32_t)c->packed_blocks[i], kw, vw, kp, vp);
 }
 
@@ -1289,7 +1378,6 @@ bdk_status bdk_adopt_block(bdk_cache* c, uint32_t b, uint32_t h, const uint16_t*
                       rec.data(), G.rec_bytes, cudaMemcpyHostToDevice),
            "H2D block");
   const int nb = slot + 1;
-  c->blocks_written = true;
   BDK_CUDA(cudaMemcpy(c->dev.packed_blocks + i, &nb, sizeof(int), cudaMemcpyHostToDevice),
            "H2D length");
   c->packed_blocks[i] = nb;
@@ -1348,7 +1436,6 @@ bdk_status bdk_corrupt_word(bdk_cache* c, uint32_t b, uint32_t h, uint32_t blk, 
   const Geom& G = c->dev.G;
   DevGuard dev_guard_(c->device);
   BDK_CUDA(cudaDeviceSynchronize(), "sync");
-  const_cast<bdk_cache*>(c)->blocks_written = true;
   BDK_CUDA(cudaMemcpy(c->dev.records + ((size_t)i * G.max_blocks + blk) * G.rec_bytes +
                           word_offset(G, word),
                       &value, 2, cudaMemcpyHostToDevice),
@@ -1641,7 +1728,6 @@ bdk_status bdk_load_cache(const uint8_t* buf, uint64_t size, uint32_t max_tokens
   }
   c->packed_blocks = nbs;
   c->res_len = rls;
-  c->blocks_written = true;
   *out = c;
   return BDK_OK;
 }

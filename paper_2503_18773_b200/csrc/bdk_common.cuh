@@ -205,6 +205,11 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// named barrier over the first n threads of the CTA (n a multiple of 32)
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
 // -------------------------------------------------------- warp reductions
 __device__ __forceinline__ float warp_max_xor(float v, int from) {
   for (int o = from; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

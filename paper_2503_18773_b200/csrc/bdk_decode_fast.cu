@@ -41,6 +41,7 @@
 
 #include "bdk_frag.cuh"
 #include "bdk_launch.h"
+#include "bdk_qpack.cuh"
 
 namespace bdk {
 
@@ -90,7 +91,7 @@ __host__ __device__ inline Smem smem_layout(const Geom& G, int ng, int NS, int g
           4 +
       64);
   L.merge_floats = merge_bytes / 4;
-  L.total = L.merge + merge_bytes + 3 * NS * 8 + 48;  // + flag, claim counters
+  L.total = L.merge + merge_bytes + 3 * NS * 8 + 48 + 128;  // + flag, claims, schedule scratch
   return L;
 }
 
@@ -98,25 +99,88 @@ __device__ __forceinline__ int cta_of_unit(long long u, long long T, int N) {
   return (int)(((u + 1) * (long long)N - 1) / T);
 }
 
-// schedule lookups: arithmetic when every cell has the same units (the host
-// sets uni_units), else the uploaded prefix arrays
-__device__ __forceinline__ long long sched_off(const FastArgs& a, int cell) {
-  return a.uni_units ? (long long)cell * a.uni_units : (long long)__ldg(a.unit_off + cell);
-}
-__device__ __forceinline__ int sched_nb(const FastArgs& a, int cell) {
-  return a.uni_units ? a.uni_nb : __ldg(a.unit_nb + cell);
-}
-
-__device__ __forceinline__ int find_cell(const int* off, int cells, long long u) {
-  int lo = 0, hi = cells - 1;  // largest c with off[c] <= u
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if ((long long)__ldg(off + mid) <= u)
-      lo = mid;
-    else
-      hi = mid - 1;
+// The step's schedule, derived on the device from the cell lengths (so a step
+// is a fixed launch, capturable in a CUDA graph).  Cell c owns nb_c packed
+// blocks of the attended range then max(1, ceil(rlen_c / rt)) residual units
+// of rt tokens.  Lengths come from the half of the double buffer that no CTA
+// writes during this step (DevCache::len2); loads bypass L1.
+struct Sched {
+  const int* pb;  // current packed block counts
+  const int* rl;  // current residual fills
+  int* pb_n;      // next step's lengths (merging CTAs write them)
+  int* rl_n;
+  int blk_begin, blk_end, rt, radd;  // radd: tokens this step appends (0/1), -1: no residual
+  __device__ __forceinline__ int nb(int cell) const {
+    return max(0, min(blk_end, __ldcg(pb + cell)) - blk_begin);
   }
-  return lo;
+  __device__ __forceinline__ int rlen(int cell) const {
+    return radd < 0 ? 0 : __ldcg(rl + cell) + radd;
+  }
+  __device__ __forceinline__ int units(int cell, int nbc) const {
+    return nbc + max(1, (rlen(cell) + rt - 1) / rt);
+  }
+};
+
+struct SchedOut {
+  long long T, off0;  // total units; first unit of cell0
+  int cell0;
+};
+
+// Block-wide scan of the cells' unit counts: total T and, for this CTA's
+// first unit u_begin = blockIdx.x * T / N, the cell holding it and that
+// cell's first unit.  All threads of the CTA; ends with __syncthreads.
+__device__ __forceinline__ SchedOut sched_scan(const Sched& S, int cells, long long* sm) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = nt >> 5;
+  const int per = (cells + nt - 1) / nt;
+  const int c0 = min(cells, tid * per), c1 = min(cells, c0 + per);
+  long long s = 0;
+  for (int cc = c0; cc < c1; ++cc) s += S.units(cc, S.nb(cc));
+  long long x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    long long w = lane < nw ? sm[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) sm[lane] = w;
+  }
+  __syncthreads();
+  const long long T = sm[nw - 1];
+  const long long excl = x - s + (warp ? sm[warp - 1] : 0);
+  // CTAs [0, min(N, T)) share the units (no empty range between two CTAs
+  // of one cell); the rest are idle
+  const long long neff = min((long long)gridDim.x, T);
+  const long long ub = (long long)blockIdx.x < neff ? (long long)blockIdx.x * T / neff : T;
+  __syncthreads();  // sm is reused for the result
+  if (s > 0 && excl <= ub && ub < excl + s) {
+    long long off = excl;
+    for (int cc = c0; cc < c1; ++cc) {
+      const long long u = S.units(cc, S.nb(cc));
+      if (ub < off + u) {
+        sm[0] = cc;
+        sm[1] = off;
+        break;
+      }
+      off += u;
+    }
+  }
+  if (ub >= T && tid == 0) {  // idle CTA (T < N)
+    sm[0] = cells;
+    sm[1] = T;
+  }
+  __syncthreads();
+  SchedOut r{T, sm[1], (int)sm[0]};
+  __syncthreads();
+  return r;
 }
 
 // next block index from a chunk position's claim counter (lane 0 claims,
@@ -562,8 +626,9 @@ struct PrepCtx {
   uint64_t* ready;
   unsigned long long* tr;
   int rec, prep_stride, pgrp;
-  long long u_begin, u_end;
+  long long u_begin, u_end, off0;
   int cell0;
+  Sched S;
 };
 
 // Prep warp: per packed block of its consumer group, fold the channel-wise K
@@ -582,12 +647,12 @@ __device__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& p
   const int h = lane % NH, cbk = lane / NH;
   const int ng = a.n_group;
   int it = 0;
-  long long u = px.u_begin;
+  long long u = px.u_begin, off = px.off0;
   for (int cell = px.cell0; u < px.u_end; ++cell) {
-    const long long ce = sched_off(a, cell + 1);
+    const int nbc = px.S.nb(cell);
+    const long long ce = off + px.S.units(cell, nbc);
     const long long seg_end = min(px.u_end, ce);
-    const long long pk_end =
-        min(seg_end, sched_off(a, cell) + sched_nb(a, cell));
+    const long long pk_end = min(seg_end, off + nbc);
     if (u < pk_end) {
       const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
       uint32_t q2[H2];
@@ -623,6 +688,7 @@ __device__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& p
       }
     }
     u = seg_end;
+    off = ce;
   }
 }
 
@@ -910,6 +976,8 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   uint64_t* ready = empty + NS;
   int* flag = reinterpret_cast<int*>(ready + NS);
   int* claim = flag + 2;  // [WN] next block per chunk position (GRP > 1)
+  long long* sched_sm =
+      reinterpret_cast<long long*>(smem + L.total - 3 * NS * 8 - 48 - 128);  // [16]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t4 = lane & 3;
   const int REC = G.rec_bytes;
 
@@ -927,66 +995,69 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   }
   __syncthreads();
 
-  const long long T = a.total_units;
-  const int N = a.n_ctas;
-  const long long u_begin = (long long)blockIdx.x * T / N;
-  const long long u_end = (long long)(blockIdx.x + 1) * T / N;
+  // ---- the step's schedule, from the device lengths (every warp waits for
+  // the previous kernel first: it may still be committing lengths)
+  if (a.pdl) pdl_wait();
+  const int par = __ldcg(c.sched) & 1;
+  Sched S;
+  S.pb = c.len2 + (size_t)par * 2 * cells;
+  S.rl = S.pb + cells;
+  S.pb_n = c.len2 + (size_t)(par ^ 1) * 2 * cells;
+  S.rl_n = S.pb_n + cells;
+  S.blk_begin = a.blk_begin;
+  S.blk_end = a.blk_end;
+  S.rt = 16 * NC;
+  S.radd = a.skip_residual ? -1 : (a.k_new != nullptr ? 1 : 0);
+  const SchedOut so = sched_scan(S, cells, sched_sm);
+  const long long T = so.T;
+  const int N = (int)min((long long)gridDim.x, T);  // CTAs sharing the units
+  const long long u_begin = (int)blockIdx.x < N ? (long long)blockIdx.x * T / N : T;
+  const long long u_end = (int)blockIdx.x < N ? (long long)(blockIdx.x + 1) * T / N : T;
   // PDL: the next kernel may start its own prologue as soon as every CTA of
   // this one is resident (the grid is one wave, so this cannot starve it)
   pdl_launch_dependents();
-  if (u_begin >= u_end) return;
-  const int cell0 =
-      a.uni_units ? (int)(u_begin / a.uni_units) : find_cell(a.unit_off, cells, u_begin);
+  const int cell0 = so.cell0;
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * 16 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
 
   // ------------------------------------------------------------ TMA warp
   if (warp == NC) {
-    if (lane == 0) {
+    if (lane == 0 && u_begin < u_end) {
       const uint64_t pol = policy_evict_first();
       int it = 0;
-      long long u = u_begin;
-      // the first NS records may stream in before the previous kernel ends
-      // (they are immutable unless that kernel was a flush); everything else
-      // waits for its memory to be visible
-      bool waited = !a.pdl;
-      if (!a.prefetch_ok && !waited) {
-        pdl_wait();
-        waited = true;
-      }
+      long long u = u_begin, off = so.off0;
       for (int cell = cell0; u < u_end; ++cell) {
-        const long long cb = sched_off(a, cell), ce = sched_off(a, cell + 1);
+        const int nbc = S.nb(cell);
+        const long long ce = off + S.units(cell, nbc);
         const long long seg_end = min(u_end, ce);
-        const long long pk_end = min(seg_end, cb + (long long)sched_nb(a, cell));
+        const long long pk_end = min(seg_end, off + nbc);
         const uint8_t* base = c.records + (size_t)cell * G.max_blocks * REC;
         for (long long x = u; x < pk_end; ++x, ++it) {
           const int s = it % NS;
-          if (!waited && it == NS) {
-            pdl_wait();
-            waited = true;
-          }
           if (it >= NS) {
             const unsigned long long tw = tr ? globaltimer() : 0ull;
             mbar_wait_sleep(&empty[s], ((it / NS) - 1) & 1);
             if (tr) tr[11] += globaltimer() - tw;
           }
           mbar_expect_tx(&full[s], (uint32_t)REC);
-          const int blk = a.blk_begin + (int)(x - cb);
+          const int blk = a.blk_begin + (int)(x - off);
           tma_bulk_g2s(ring + (size_t)s * REC, base + (size_t)blk * REC, (uint32_t)REC, &full[s],
                        pol);
         }
         u = seg_end;
+        off = ce;
       }
     }
     return;
   }
 
   // ---------------------------------------------------------- prep warps
-  if (a.pdl && warp != NC) pdl_wait();  // q, cache state, counters, slots
   if (warp > NC) {
+    if (u_begin >= u_end) return;
     const int pgrp = warp - NC - 1;  // prepares the blocks of consumer group pgrp
     const int nh = ng <= 1 ? 1 : ng <= 2 ? 2 : ng <= 4 ? 4 : 8;
-    PrepCtx px{ring, prep, full, ready, tr, REC, (int)L.prep_stride, pgrp, u_begin, u_end, cell0};
+    PrepCtx px{ring, prep, full, ready, tr, REC, (int)L.prep_stride, pgrp, u_begin, u_end,
+               so.off0, cell0, S};
     if (nh == 1) prep_loop<1, NS, GRP>(c, a, px);
     else if (nh == 2) prep_loop<2, NS, GRP>(c, a, px);
     else if (nh == 4) prep_loop<4, NS, GRP>(c, a, px);
@@ -1014,11 +1085,12 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   const int stride_slot = slot_stride(ng);
 
   int it = 0;
-  long long u = u_begin;
+  long long u = u_begin, off = so.off0;
   for (int cell = cell0; u < u_end; ++cell) {
-    const long long cb = sched_off(a, cell), ce = sched_off(a, cell + 1);
+    const int nbc = S.nb(cell);
+    const long long cb = off, ce = off + S.units(cell, nbc);
     const long long seg_end = min(u_end, ce);
-    const long long res_begin = cb + (long long)sched_nb(a, cell);  // 1st residual unit
+    const long long res_begin = cb + nbc;  // 1st residual unit
     const long long pk_end = min(seg_end, res_begin);
     Soft st{-INFINITY, -INFINITY, 0.f, 0.f, 0.f, 0.f};
     float o[OT][4];  // O^T (subnormal-mode scaled, see oscale)
@@ -1057,6 +1129,8 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     // ---------------- residual window (fp16), append fused.  Residual unit r
     // of a cell covers tokens [r*RT, (r+1)*RT) (RT = 16 per consumer warp);
     // the CTA whose range holds row res_len writes the new token there.
+    const int rl0 = __ldcg(S.rl + cell);
+    const bool app = a.k_new != nullptr && !a.skip_residual;
     float oscale_seg = oscale;
     if (seg_end > res_begin && !a.skip_residual) {
       // the packed-block O is held at scale 2^(SH_REF - 24) (subnormal-mode
@@ -1070,8 +1144,6 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       }
       oscale_seg = 1.f;
       constexpr int RT = 16 * NC;
-      const int rl0 = c.res_len[cell];
-      const bool app = a.k_new != nullptr;
       const int rlen = rl0 + (app ? 1 : 0);
       const int t_lo = (int)(max(u, res_begin) - res_begin) * RT;
       const int t_hi = min(rlen, (int)(seg_end - res_begin) * RT);
@@ -1089,25 +1161,39 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       // thread by the barrier) and acquire the other contributors' slots
       const int prev = atom_add_acq_rel_gpu(a.counters + cell, 1);
       const int last = prev == hi - lo;
-      if (last) {
-        a.counters[cell] = 0;
-        // commit the append once every contributor has read res_len
-        if (a.k_new != nullptr && !a.skip_residual) c.res_len[cell] = c.res_len[cell] + 1;
-      }
-      *flag = last;
+      if (last) a.counters[cell] = 0;
+      // the step's commit of this cell (merging CTA, after every contributor
+      // has read the window): 1 = lengths carried over (+ the append),
+      // 2 = the append filled the window -> flush it into a new block
+      flag[0] = !last ? 0 : (app && rl0 + 1 == G.n_r) ? 2 : 1;
     }
     named_bar(1, NC * 32);
     if (tr && threadIdx.x == 0) tr[10] = globaltimer();
-    if (*flag) {
+    const int commit = flag[0];
+    if (commit) {
       const float* base = a.slots + (size_t)(lo + cell) * stride_slot;
       if (hi - lo + 1 <= MERGE_KC_FEW)
         merge_cell_few<NC>(a, G, cell, base, hi - lo + 1, merge_sm, tr);
       else
         merge_cell<NC>(a, G, cell, base, hi - lo + 1, merge_sm, tr);
+      const int pb0 = __ldcg(S.pb + cell);
+      if (commit == 2) {
+        // build_block + commit_block (kvcache.cpp:208-237) after the step's
+        // attention (attention.cpp:235-240): quantize + pack the full window
+        // into the cell's next block slot
+        named_bar(1, NC * 32);
+        const size_t wo = (size_t)cell * G.n_r * D;
+        flush_window<BITS>(G, c.res_k + wo, c.res_v + wo,
+                           c.records + ((size_t)cell * G.max_blocks + pb0) * REC, NC * 32, 1);
+      }
+      if (threadIdx.x == 0) {
+        S.pb_n[cell] = commit == 2 ? pb0 + 1 : pb0;
+        S.rl_n[cell] = commit == 2 ? 0 : rl0 + (app ? 1 : 0);
+      }
     }
     if (tr && threadIdx.x == 0) {
       tr[5] = globaltimer();
-      tr[6] = (unsigned long long)(*flag);
+      tr[6] = (unsigned long long)(commit != 0);
       tr[7] = (unsigned long long)(u_end - u_begin);
       unsigned int smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -1118,9 +1204,18 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     if (GRP > 1 && threadIdx.x < WN) claim[threadIdx.x] = it;
     named_bar(1, NC * 32);  // flag / merge smem reuse by the next segment
     u = seg_end;
+    off = ce;
+  }
+  // ---- step end: the last CTA to finish bumps the step, so the next launch
+  // reads the lengths this one's merging CTAs wrote (every cell has a merge)
+  if (threadIdx.x == 0) {
+    const int prev = atom_add_acq_rel_gpu(c.sched + 1, 1);
+    if (prev == (int)gridDim.x - 1) {
+      c.sched[1] = 0;
+      c.sched[0] = c.sched[0] + 1;
+    }
   }
 }
-
 
 }  // namespace
 

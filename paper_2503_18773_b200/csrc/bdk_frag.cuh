@@ -43,9 +43,6 @@ __device__ __forceinline__ __half2 ext(uint32_t r, uint32_t r8) {
 }
 
 
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
-}
 
 }  // namespace bdk
 

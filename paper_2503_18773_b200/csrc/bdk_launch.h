@@ -15,8 +15,17 @@ struct DevCache {
   uint8_t* records = nullptr;  // [cells][max_blocks][rec_bytes]
   __half* res_k = nullptr;     // [cells][n_r][d]
   __half* res_v = nullptr;
+  // current lengths (the host points these at the live half of len2 before
+  // every launch; kernels other than the fast decode update them in place)
   int* packed_blocks = nullptr;  // [cells]
   int* res_len = nullptr;        // [cells]
+  // double-buffered lengths of the fast decode: [2][packed_blocks | res_len][cells].
+  // A fast step reads half (step & 1) and its merging CTAs write every cell's
+  // next lengths into the other half; the last CTA to exit bumps the step.
+  // So the schedule is read from memory nothing writes during the step, and
+  // a step is a fixed launch (capturable in a CUDA graph).
+  int* len2 = nullptr;
+  int* sched = nullptr;  // [0] step (fast decode launches), [1] CTAs exited this step
 };
 
 struct DecodeArgs {
@@ -48,19 +57,13 @@ struct FastArgs {
   float* out_lse = nullptr;  // optional [batch][heads_q] (log2 domain)
   float* slots = nullptr;    // [n_ctas + cells][n_group][d + 2] partials
   int* counters = nullptr;   // [cells], zero between launches
-  const int* unit_off = nullptr;  // [cells + 1] prefix sum of units per cell
-  const int* unit_nb = nullptr;   // [cells] packed-block units of each cell (the
-                                  // rest are residual units of 16*warp_n tokens)
-  long long total_units = 0;
-  int uni_units = 0, uni_nb = 0;  // every cell: uni_units units, uni_nb packed (0: use arrays)
-  int n_ctas = 0, heads_q = 0, n_group = 0, blk_begin = 0;
+  int n_ctas = 0, heads_q = 0, n_group = 0;
+  int blk_begin = 0, blk_end = 1 << 30;  // packed block range attended
   int skip_residual = 0;  // residual units attend nothing (sequence-split ranks)
   float sm_scale_log2 = 0.f;
   unsigned long long* trace = nullptr;  // dev: [n_ctas][16] globaltimer stamps
   int dev_flags = 0;                    // dev probes (BDK_DEV_FLAGS): 1 no compute, 2 no prep
-  int pdl = 0;          // launched as a programmatic dependent of the previous kernel
-  int prefetch_ok = 0;  // packed records unchanged since the previous kernel: the
-                        // TMA warp may prefetch them before griddepcontrol.wait
+  int pdl = 0;  // launched as a programmatic dependent of the previous kernel
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
 };
 

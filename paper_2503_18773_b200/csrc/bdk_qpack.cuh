@@ -210,4 +210,123 @@ __device__ inline void qpack_block(const Geom& G, const __half* k, const __half*
   }
 }
 
+// Fused flush of one full residual window (build_block + commit_block,
+// kvcache.cpp:208-237) by a CTA that has other warps busy or gone: threads
+// [0, nthr) only, synchronized by named barrier `bar` (nthr threads), no
+// shared memory.  Geometry of the fast decode kernel: KChannel K with
+// g | N_r, per-token V groups of g = d (one (scale, zero) per token).
+// Same arithmetic as qpass_channel / qpass_token / qpass_pack (bit-exact
+// with the reference): K item (c, gr) scans its g tokens in order; V token t
+// reduces its row per warp with the first-zero sign rule; codes are packed
+// straight into the swizzled word rows (thread per channel row), the V
+// params read back from the record the first pass wrote.
+template <int BITS>
+__device__ __noinline__ void flush_window(const Geom& G, const __half* rk, const __half* rv,
+                                    uint8_t* rec, int nthr, int bar) {
+  constexpr int P = 16 / BITS;
+  const float qmax = static_cast<float>((1u << BITS) - 1u);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+  const int d = G.d, n_r = G.n_r, g = G.g, rb = 16 * G.warp_n;
+  uint8_t* kw = rec;
+  uint8_t* vw = rec + G.wbytes;
+  uint32_t* kp = reinterpret_cast<uint32_t*>(rec + 2 * G.wbytes);
+  uint32_t* vp = reinterpret_cast<uint32_t*>(rec + 2 * G.wbytes + G.kp_bytes);
+  int tok[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) tok[p] = pos_token(p, P, G.interleave);
+  // ---- K: thread per (channel, group): params, then its words
+  const int ngr = n_r / g, wpg = g / P;  // words per group in a row
+  for (int it = tid; it < d * ngr; it += nthr) {
+    const int c = it % d, gr = it / d;
+    const __half* col = rk + (size_t)gr * g * d + c;
+    float lo = __half2float(col[0]), hi = lo;
+    for (int i = 0; i < g; ++i) {
+      const float x = __half2float(col[(size_t)i * d]);
+      lo = x < lo ? x : lo;  // std::min(lo, x)
+      hi = hi < x ? x : hi;  // std::max(hi, x)
+    }
+    float sc, z;
+    group_params(lo, hi, qmax, sc, z);
+    kp[gr * d + c] = param_u32(sc, z);
+    for (int w8 = 0; w8 < wpg; w8 += 8) {  // one 16-byte chunk: 8 words
+      uint32_t q4[4];
+#pragma unroll
+      for (int i2 = 0; i2 < 4; ++i2) {
+        uint32_t pair = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int wi = gr * wpg + w8 + 2 * i2 + h;  // word index in the row
+          uint32_t word = 0;
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            const float x = __half2float(rk[(size_t)(wi * P + tok[p]) * d + c]);
+            word |= quant_code(x, sc, z, qmax) << (p * BITS);
+          }
+          pair |= word << (16 * h);
+        }
+        q4[i2] = pair;
+      }
+      const int j = (gr * wpg + w8) / 8;
+      *reinterpret_cast<uint4*>(kw + (size_t)c * rb + ((j ^ swz(c, G.warp_n)) << 4)) =
+          make_uint4(q4[0], q4[1], q4[2], q4[3]);
+    }
+  }
+  // ---- V params: warp per token, lanes over channels (qpass_token, g >= 32)
+  const int groups = d / g, ipg = g / 32;
+  for (int t = warp; t < n_r; t += nwarps) {
+    const __half* row = rv + (size_t)t * d;
+    for (int gc = 0; gc < groups; ++gc) {
+      float lo = INFINITY, hi = -INFINITY;
+      int zfirst = 0x7fffffff;
+      for (int i = 0; i < ipg; ++i) {
+        const int c = gc * g + i * 32 + lane;
+        const float x = __half2float(row[c]);
+        lo = fminf(lo, x);
+        hi = fmaxf(hi, x);
+        if (x == 0.0f) zfirst = min(zfirst, c);
+      }
+      for (int o = 16; o >= 1; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        zfirst = min(zfirst, __shfl_xor_sync(0xffffffffu, zfirst, o));
+      }
+      if (lo == 0.0f) lo = __half2float(row[zfirst]);
+      if (hi == 0.0f) hi = __half2float(row[zfirst]);
+      float sc, z;
+      group_params(lo, hi, qmax, sc, z);
+      if (lane == 0) vp[t * groups + gc] = param_u32(sc, z);
+    }
+  }
+  named_bar(bar, nthr);  // V params visible to every thread of the flush
+  // ---- V words: thread per channel row, codes with the token's params
+  for (int c = tid; c < d; c += nthr) {
+    const int gc = c / g;
+    for (int j = 0; j < G.warp_n; ++j) {
+      uint32_t q4[4];
+#pragma unroll
+      for (int i2 = 0; i2 < 4; ++i2) {
+        uint32_t pair = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int wi = j * 8 + 2 * i2 + h;
+          uint32_t word = 0;
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            const int t = wi * P + tok[p];
+            const uint32_t pr = vp[t * groups + gc];
+            const float sc = __half2float(__ushort_as_half(static_cast<uint16_t>(pr & 0xFFFFu)));
+            const float z = __half2float(__ushort_as_half(static_cast<uint16_t>(pr >> 16)));
+            word |= quant_code(__half2float(rv[(size_t)t * d + c]), sc, z, qmax) << (p * BITS);
+          }
+          pair |= word << (16 * h);
+        }
+        q4[i2] = pair;
+      }
+      *reinterpret_cast<uint4*>(vw + (size_t)c * rb + ((j ^ swz(c, G.warp_n)) << 4)) =
+          make_uint4(q4[0], q4[1], q4[2], q4[3]);
+    }
+  }
+  named_bar(bar, nthr);
+}
+
 }  // namespace bdk
