@@ -125,6 +125,13 @@ struct SchedOut {
   long long T, off0;  // total units; first unit of cell0
   int cell0;
 };
+__device__ __forceinline__ int cell0_of(const SchedOut& so) { return so.cell0; }
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // Block-wide scan of the cells' unit counts: total T and, for this CTA's
 // first unit u_begin = blockIdx.x * T / N, the cell holding it and that
@@ -629,6 +636,7 @@ struct PrepCtx {
   long long u_begin, u_end, off0;
   int cell0;
   Sched S;
+  int redo, pf;  // full-barrier phase offset of the first pf stages (see full_par)
 };
 
 // Prep warp: per packed block of its consumer group, fold the channel-wise K
@@ -675,7 +683,7 @@ __device__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& p
         if (GRP > 1 && (it % GRP) != px.pgrp) continue;
         const int s = it % NS;
         const unsigned long long tw = (px.tr && lane == 0) ? globaltimer() : 0ull;
-        mbar_wait_sleep(&px.full[s], (it / NS) & 1);
+        mbar_wait_sleep(&px.full[s], ((it / NS) + ((px.redo && s < px.pf) ? 1 : 0)) & 1);
         const unsigned long long tb = (px.tr && lane == 0) ? globaltimer() : 0ull;
         if (px.tr && lane == 0) px.tr[12] += tb - tw;
         if (!(a.dev_flags & 2)) {
@@ -995,27 +1003,91 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   }
   __syncthreads();
 
-  // ---- the step's schedule, from the device lengths (every warp waits for
-  // the previous kernel first: it may still be committing lengths)
-  if (a.pdl) pdl_wait();
-  const int par = __ldcg(c.sched) & 1;
+  // PDL: the next kernel may launch its CTAs as soon as every CTA of this one
+  // is resident (the grid is one wave, so this cannot starve it)
+  pdl_launch_dependents();
+  // ---- the step's schedule, from the device lengths.  Under PDL the
+  // previous step may still be committing them: read the step counter and
+  // its half of the lengths now (speculation), let the TMA warp stream the
+  // first records of that schedule, and verify after griddepcontrol.wait --
+  // the schedule stands unless the previous step changed some cell's unit
+  // count, which its merging CTAs flag per half (sched[2 + half]).
   Sched S;
-  S.pb = c.len2 + (size_t)par * 2 * cells;
-  S.rl = S.pb + cells;
-  S.pb_n = c.len2 + (size_t)(par ^ 1) * 2 * cells;
-  S.rl_n = S.pb_n + cells;
   S.blk_begin = a.blk_begin;
   S.blk_end = a.blk_end;
   S.rt = 16 * NC;
   S.radd = a.skip_residual ? -1 : (a.k_new != nullptr ? 1 : 0);
-  const SchedOut so = sched_scan(S, cells, sched_sm);
-  const long long T = so.T;
-  const int N = (int)min((long long)gridDim.x, T);  // CTAs sharing the units
-  const long long u_begin = (int)blockIdx.x < N ? (long long)blockIdx.x * T / N : T;
-  const long long u_end = (int)blockIdx.x < N ? (long long)(blockIdx.x + 1) * T / N : T;
-  // PDL: the next kernel may start its own prologue as soon as every CTA of
-  // this one is resident (the grid is one wave, so this cannot starve it)
-  pdl_launch_dependents();
+  auto bind = [&](int step) {
+    const int par = step & 1;
+    S.pb = c.len2 + (size_t)par * 2 * cells;
+    S.rl = S.pb + cells;
+    S.pb_n = c.len2 + (size_t)(par ^ 1) * 2 * cells;
+    S.rl_n = S.pb_n + cells;
+  };
+  const int s0 = ld_acquire_gpu(c.sched);
+  bind(s0);
+  SchedOut so = sched_scan(S, cells, sched_sm);
+  long long T = so.T;
+  int N = (int)min((long long)gridDim.x, T);  // CTAs sharing the units
+  long long u_begin = (int)blockIdx.x < N ? (long long)blockIdx.x * T / N : T;
+  long long u_end = (int)blockIdx.x < N ? (long long)(blockIdx.x + 1) * T / N : T;
+  const uint64_t pol = policy_evict_first();
+  int pf = 0;  // records the TMA warp streamed on the speculative schedule
+  if (a.pdl && warp == NC && lane == 0) {
+    // only records at least two blocks behind a cell's newest one: older
+    // records are immutable whatever the previous step still writes
+    long long u = u_begin, off = so.off0;
+    for (int cell = cell0_of(so); u < u_end && pf < NS; ++cell) {
+      const int nbc = S.nb(cell);
+      const long long ce = off + S.units(cell, nbc);
+      const long long pk_end = min(min(u_end, ce), off + nbc);
+      const int pb_safe = __ldcg(S.pb + cell) - 2;
+      const uint8_t* base = c.records + (size_t)cell * G.max_blocks * REC;
+      for (long long x = u; x < pk_end && pf < NS; ++x) {
+        const int blk = a.blk_begin + (int)(x - off);
+        if (blk >= pb_safe) {
+          u = u_end;  // stop speculating (keeps the sequence a prefix)
+          break;
+        }
+        mbar_expect_tx(&full[pf], (uint32_t)REC);
+        tma_bulk_g2s(ring + (size_t)pf * REC, base + (size_t)blk * REC, (uint32_t)REC, &full[pf],
+                     pol);
+        ++pf;
+      }
+      if (u >= u_end) break;
+      u = min(u_end, ce);
+      off = ce;
+    }
+    sched_sm[14] = pf;
+  }
+  int redo = 0;
+  if (a.pdl) {
+    pdl_wait();
+    if (threadIdx.x == 0) {
+      const int s1 = __ldcg(c.sched);
+      const int ok = s1 == s0 || (s1 == s0 + 1 && __ldcg(c.sched + 2 + (s1 & 1)) == 0);
+      sched_sm[15] = ok ? 0 : s1 + 1;
+    }
+    __syncthreads();
+    pf = (int)sched_sm[14];
+    redo = sched_sm[15] != 0;
+    if (redo) {  // the previous step moved the schedule: rescan its lengths
+      const int s1 = (int)sched_sm[15] - 1;
+      __syncthreads();  // sched_sm reused by the scan
+      bind(s1);
+      so = sched_scan(S, cells, sched_sm);
+      T = so.T;
+      N = (int)min((long long)gridDim.x, T);
+      u_begin = (int)blockIdx.x < N ? (long long)blockIdx.x * T / N : T;
+      u_end = (int)blockIdx.x < N ? (long long)(blockIdx.x + 1) * T / N : T;
+    }
+  }
+  const int par_cur = (int)(S.pb - c.len2) / (2 * cells);
+  // full-barrier phase of ring iteration k at stage s: a stage that held a
+  // discarded speculative record completed one extra phase
+  auto full_par = [&](int k) -> uint32_t {
+    return (uint32_t)((k / NS) + ((redo && (k % NS) < pf) ? 1 : 0)) & 1u;
+  };
   const int cell0 = so.cell0;
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * 16 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
@@ -1023,7 +1095,10 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   // ------------------------------------------------------------ TMA warp
   if (warp == NC) {
     if (lane == 0 && u_begin < u_end) {
-      const uint64_t pol = policy_evict_first();
+      // a rescheduled step discards the speculative records: let them land
+      // (their stages then complete one extra phase, see full_par)
+      if (redo)
+        for (int s = 0; s < pf; ++s) mbar_wait(&full[s], 0);
       int it = 0;
       long long u = u_begin, off = so.off0;
       for (int cell = cell0; u < u_end; ++cell) {
@@ -1034,6 +1109,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
         const uint8_t* base = c.records + (size_t)cell * G.max_blocks * REC;
         for (long long x = u; x < pk_end; ++x, ++it) {
           const int s = it % NS;
+          if (!redo && it < pf) continue;  // streamed before griddepcontrol.wait
           if (it >= NS) {
             const unsigned long long tw = tr ? globaltimer() : 0ull;
             mbar_wait_sleep(&empty[s], ((it / NS) - 1) & 1);
@@ -1057,7 +1133,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     const int pgrp = warp - NC - 1;  // prepares the blocks of consumer group pgrp
     const int nh = ng <= 1 ? 1 : ng <= 2 ? 2 : ng <= 4 ? 4 : 8;
     PrepCtx px{ring, prep, full, ready, tr, REC, (int)L.prep_stride, pgrp, u_begin, u_end,
-               so.off0, cell0, S};
+               so.off0, cell0, S, redo, pf};
     if (nh == 1) prep_loop<1, NS, GRP>(c, a, px);
     else if (nh == 2) prep_loop<2, NS, GRP>(c, a, px);
     else if (nh == 4) prep_loop<4, NS, GRP>(c, a, px);
@@ -1109,7 +1185,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       unsigned long long tw = 0;
       if (tr && threadIdx.x == 0) tw = globaltimer();
       mbar_wait(&ready[s], (k / NS) & 1);
-      mbar_wait(&full[s], (k / NS) & 1);
+      mbar_wait(&full[s], full_par(k));
       if (tr && threadIdx.x == 0) {
         const unsigned long long now = globaltimer();
         if (k == 0) tr[1] = now; else tr[9] += now - tw;
@@ -1187,8 +1263,16 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
                            c.records + ((size_t)cell * G.max_blocks + pb0) * REC, NC * 32, 1);
       }
       if (threadIdx.x == 0) {
-        S.pb_n[cell] = commit == 2 ? pb0 + 1 : pb0;
-        S.rl_n[cell] = commit == 2 ? 0 : rl0 + (app ? 1 : 0);
+        const int pbn = commit == 2 ? pb0 + 1 : pb0;
+        const int rln = commit == 2 ? 0 : rl0 + (app ? 1 : 0);
+        S.pb_n[cell] = pbn;
+        S.rl_n[cell] = rln;
+        // does the next launch (appending or not) see a different unit count
+        // for this cell?  Then a speculative schedule read from this step's
+        // half is stale (the flag of the half just written)
+        auto nres = [&](int r) { return max(1, (r + S.rt - 1) / S.rt); };
+        if (pbn != pb0 || nres(rln) != nres(rl0) || nres(rln + 1) != nres(rl0 + 1))
+          atomicOr(c.sched + 2 + (par_cur ^ 1), 1);
       }
     }
     if (tr && threadIdx.x == 0) {
@@ -1212,6 +1296,8 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     const int prev = atom_add_acq_rel_gpu(c.sched + 1, 1);
     if (prev == (int)gridDim.x - 1) {
       c.sched[1] = 0;
+      c.sched[2 + par_cur] = 0;  // the half the next step writes starts unflagged
+      __threadfence();           // lengths + flags before the step (speculative readers)
       c.sched[0] = c.sched[0] + 1;
     }
   }
