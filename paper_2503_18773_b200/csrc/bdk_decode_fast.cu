@@ -1063,20 +1063,17 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   int redo = 0;
   if (a.pdl) {
     pdl_wait();
-    if (threadIdx.x == 0) {
-      const int s1 = __ldcg(c.sched);
-      const int ok = s1 == s0 || (s1 == s0 + 1 && __ldcg(c.sched + 2 + (s1 & 1)) == 0);
-      sched_sm[13] = s1;
-      sched_sm[15] = ok ? 0 : 1;
-    }
-    __syncthreads();
-    pf = (int)sched_sm[14];
-    redo = sched_sm[15] != 0;
+    // every thread reads the same final words, so the outcome is CTA-uniform
+    // and the common (valid) path needs no barrier after the wait
+    const int s1 = __ldcg(c.sched);
+    const int ok = s1 == s0 || (s1 == s0 + 1 && __ldcg(c.sched + 2 + (s1 & 1)) == 0);
     // the lengths this step reads and writes are always the final half; a
     // valid speculation only means the unit counts (the schedule) agree
-    bind((int)sched_sm[13]);
-    if (redo) {  // the previous step moved the schedule: rescan its lengths
-      __syncthreads();  // sched_sm reused by the scan
+    bind(s1);
+    if (!ok) {  // the previous step moved the schedule: rescan its lengths
+      redo = 1;
+      __syncthreads();  // publishes pf (TMA lane); sched_sm is reused by the scan
+      pf = (int)sched_sm[14];
       so = sched_scan(S, cells, sched_sm);
       T = so.T;
       N = (int)min((long long)gridDim.x, T);
