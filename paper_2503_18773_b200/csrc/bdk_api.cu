@@ -45,8 +45,11 @@ struct bdk_cache {
   void* d_stage = nullptr;
   size_t stage_bytes = 0;
   // fast-path (stream-K) resources
-  uint64_t fast_steps = 0;            // fast decode launches (= the device step counter)
+  uint64_t fast_steps = 0;            // fast decode steps (their parity picks the len2 half)
   bool capturing_pdl_off = false;     // graph capture without programmatic launch edges
+  int* unit_off = nullptr;            // device host-schedule [unit_off (cells + 1) | unit_nb (cells)]
+  std::vector<int> unit_off_host;     // last uploaded host schedule
+  bool blocks_written = true;         // a packed record may have changed since the last fast step
   int* counters = nullptr;            // device [cells]
   int graphs = 0;                     // live bdk_graph objects (workspaces are pinned)
   float* slots = nullptr;             // device partial slots
@@ -230,13 +233,16 @@ void point_lengths(bdk_cache* c) {
 }
 
 // mirror of one fast step's commit: every cell +1 token when it appends, a
-// full window becomes a block; the device step counter moved to the other half
+// full window becomes a block (written by the step's merging CTA); the
+// lengths now live in the other half of len2
 void advance_fast_step(bdk_cache* c, bool appends) {
+  c->blocks_written = false;
   if (appends) {
     for (size_t i = 0; i < c->res_len.size(); ++i) {
       if (++c->res_len[i] == c->dev.G.n_r) {
         c->res_len[i] = 0;
         c->packed_blocks[i] += 1;
+        c->blocks_written = true;
       }
     }
   }
@@ -245,14 +251,16 @@ void advance_fast_step(bdk_cache* c, bool appends) {
 }
 
 // Stream-K fast path (bdk_decode_fast.cu): ONE launch per step -- append,
-// attention, combine and the flush of any residual the step fills -- with the
-// schedule derived on the device from the double-buffered lengths, so the
-// launch arguments never change from step to step (a captured CUDA graph of
-// steps replays correctly).  The host mirror follows the same length
-// arithmetic for the reference's precondition checks.
+// attention, combine and the flush of any residual the step fills.  Eager
+// steps take their schedule from the host mirror of the lengths (arguments,
+// plus an upload when it is not uniform and changed); graph-captured steps
+// (dev_sched) scan the device lengths instead, so their arguments hold for any
+// lengths and a captured graph of steps replays correctly.  Both give the
+// same unit partition, hence bit-identical results.
 bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void* q,
                            const void* k_new, const void* v_new, float* out, float* lse,
-                           int blk_begin, int blk_end, cudaStream_t stream, bool no_res) {
+                           int blk_begin, int blk_end, cudaStream_t stream, bool no_res,
+                           bool dev_sched = false) {
   const int cells = static_cast<int>(c->desc.batch * c->desc.heads_kv);
   const int ng = static_cast<int>(cfg->heads_q / cfg->heads_kv);
   const Geom& G = c->dev.G;
@@ -295,6 +303,50 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
   a.blk_end = blk_end;
   a.skip_residual = no_res ? 1 : 0;
   a.sm_scale_log2 = (1.0f / std::sqrt(static_cast<float>(cfg->head_dim))) * bdk::kLog2e;
+  a.par = static_cast<int>(c->fast_steps & 1);
+  static const bool dev_sched_knob = getenv("BDK_DEVSCHED") && atoi(getenv("BDK_DEVSCHED")) == 1;
+  if (dev_sched_knob) dev_sched = true;
+  a.dev_sched = dev_sched ? 1 : 0;
+  if (!dev_sched) {
+    // schedule: [unit_off (cells + 1) | unit_nb (cells)]; a cell's units are
+    // its packed blocks in range then ceil(res_len' / rt) residual units
+    const int rt = bdk::fast_residual_tokens(G);
+    std::vector<int> off(2 * cells + 1, 0);
+    for (int i = 0; i < cells; ++i) {
+      const int nb = std::max(0, std::min(blk_end, c->packed_blocks[i]) - blk_begin);
+      const int rlen = no_res ? 0 : c->res_len[i] + (k_new != nullptr ? 1 : 0);
+      off[i + 1] = off[i] + nb + std::max(1, (rlen + rt - 1) / rt);
+      off[cells + 1 + i] = nb;
+    }
+    bool uni = true;
+    for (int i = 1; i < cells && uni; ++i)
+      uni = off[i + 1] - off[i] == off[1] - off[0] && off[cells + 1 + i] == off[cells + 1];
+    a.total_units = off[cells];
+    a.uni_units = uni ? off[1] - off[0] : 0;
+    a.uni_nb = uni ? off[cells + 1] : 0;
+    bool uni_len = true;
+    for (int i = 1; i < cells && uni_len; ++i)
+      uni_len = c->packed_blocks[i] == c->packed_blocks[0] && c->res_len[i] == c->res_len[0];
+    a.uni_len = uni_len ? 1 : 0;
+    a.uni_pb = c->packed_blocks[0];
+    a.uni_rl = c->res_len[0];
+    if (!uni) {
+      if (!c->unit_off)
+        BDK_CUDA(cudaMalloc(&c->unit_off, (2 * cells + 1) * sizeof(int)), "cudaMalloc(schedule)");
+      if (off != c->unit_off_host) {
+        BDK_CUDA(cudaMemcpyAsync(c->unit_off, off.data(), (2 * cells + 1) * sizeof(int),
+                                 cudaMemcpyHostToDevice, stream),
+                 "H2D schedule");
+        c->unit_off_host = off;
+      }
+      a.unit_off = c->unit_off;
+      a.unit_nb = c->unit_off + cells + 1;
+    }
+  }
+  // the first ring stages may stream before the previous kernel ends when no
+  // packed record changed since the last fast step (dev knob BDK_PREFETCH=0)
+  static const bool prefetch_off = getenv("BDK_PREFETCH") && atoi(getenv("BDK_PREFETCH")) == 0;
+  a.prefetch_ok = (c->blocks_written || prefetch_off) ? 0 : 1;
   bdk_status st = next_events(c, &a.ev_begin, &a.ev_end);
   if (st) return st;
   // dev knob: BDK_TRACE=<file> appends per-CTA globaltimer stamps of every
@@ -394,6 +446,7 @@ bdk_status run_decode_span(bdk_cache* c, const bdk_attn_config* cfg, const void*
                                     k_new != nullptr ? c->dev.res_len : nullptr, stream),
            "span combine launch");
   c->launches += 2;
+  c->blocks_written = true;  // packed records may change (no PDL prefetch next)
   if (k_new != nullptr) {
     bool full = false;
     for (int i = 0; i < cells; ++i) full |= c->res_len[i] + 1 == c->dev.G.n_r;
@@ -461,6 +514,7 @@ bdk_status run_decode(bdk_cache* c, const bdk_attn_config* cfg, const void* q, c
     if (st) return st;
   }
   BDK_CUDA(bdk::launch_decode(c->dev, a, stream), "decode launch");
+  c->blocks_written = true;  // packed records may change (no PDL prefetch next)
   c->launches += 2;  // split-KV kernel + combine kernel
   if (k_new != nullptr) {  // mirror of the cache-update phase
     for (int i = 0; i < cells; ++i) {
@@ -564,9 +618,7 @@ bdk_status bdk_cache_create(const bdk_cache_desc* d, bdk_cache** out) {
   if (e == cudaSuccess) e = cudaMalloc(&c->dev.res_k, cells * n_r * d->head_dim * 2);
   if (e == cudaSuccess) e = cudaMalloc(&c->dev.res_v, cells * n_r * d->head_dim * 2);
   if (e == cudaSuccess) e = cudaMalloc(&c->dev.len2, 4 * cells * sizeof(int));
-  if (e == cudaSuccess) e = cudaMalloc(&c->dev.sched, 16 * sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(c->dev.len2, 0, 4 * cells * sizeof(int));
-  if (e == cudaSuccess) e = cudaMemset(c->dev.sched, 0, 16 * sizeof(int));
   point_lengths(c);
   if (e != cudaSuccess) {
     bdk_cache_destroy(c);
@@ -583,7 +635,7 @@ bdk_status bdk_cache_destroy(bdk_cache* c) {
   cudaFree(c->dev.res_k);
   cudaFree(c->dev.res_v);
   cudaFree(c->dev.len2);
-  cudaFree(c->dev.sched);
+  cudaFree(c->unit_off);
   cudaFree(c->part_o);
   cudaFree(c->part_ml);
   cudaFree(c->span_parts);
@@ -632,6 +684,7 @@ bdk_status bdk_prefill(bdk_cache* c, uint32_t b, uint32_t h, const void* k, cons
   const int nb = static_cast<int>(len / c->dev.G.n_r);
   if (nb > c->dev.G.max_blocks) return fail(BDK_CAPACITY_ERROR, "prefill exceeds max_tokens");
   if (len > 0 && (!k || !v)) return fail(BDK_INVALID_ARGUMENT, "null k/v");
+  c->blocks_written = true;  // packed records may change (no PDL prefetch next)
   DevGuard dev_guard_(c->device);
   c->launches += 1;
   BDK_CUDA(bdk::launch_prefill(c->dev, static_cast<const __half*>(k),
@@ -653,6 +706,7 @@ bdk_status bdk_cache_reset(bdk_cache* c, void* stream) {
            "reset res_len");
   std::fill(c->packed_blocks.begin(), c->packed_blocks.end(), 0);
   std::fill(c->res_len.begin(), c->res_len.end(), 0);
+  c->blocks_written = true;
   return BDK_OK;
 }
 
@@ -664,6 +718,7 @@ bdk_status bdk_prefill_all(bdk_cache* c, const void* k, const void* v, uint32_t 
       return fail(BDK_STATE_ERROR, "prefill into a non-empty cell");
   const int nb = static_cast<int>(len / c->dev.G.n_r);
   if (nb > c->dev.G.max_blocks) return fail(BDK_CAPACITY_ERROR, "prefill exceeds max_tokens");
+  c->blocks_written = true;  // packed records may change (no PDL prefetch next)
   const int cells = static_cast<int>(c->res_len.size());
   DevGuard dev_guard_(c->device);
   c->launches += 1;
@@ -683,6 +738,7 @@ bdk_status bdk_append_token(bdk_cache* c, uint32_t b, uint32_t h, const void* k,
   bdk_status s = check_cell(c, b, h);
   if (s) return s;
   const int i = cell_of(c, b, h);
+  c->blocks_written = true;  // packed records may change (no PDL prefetch next)
   if (c->res_len[i] == c->dev.G.n_r)
     return fail(BDK_CAPACITY_ERROR, "residual is full; flush before appending");
   DevGuard dev_guard_(c->device);
@@ -706,6 +762,7 @@ bdk_status bdk_flush_residual(bdk_cache* c, uint32_t b, uint32_t h, void* stream
   DevGuard dev_guard_(c->device);
   c->launches += 1;
   BDK_CUDA(bdk::launch_flush(c->dev, i, as_stream(stream)), "flush launch");
+  c->blocks_written = true;
   c->packed_blocks[i] += 1;
   c->res_len[i] = 0;
   return BDK_OK;
@@ -738,7 +795,7 @@ bdk_status bdk_decode_partial(bdk_cache* c, const bdk_attn_config* cfg, const vo
 
 struct bdk_graph {
   bdk_cache* cache = nullptr;
-  cudaGraphExec_t exec = nullptr;
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};  // by the parity of the first step
   uint32_t n_steps = 0;
 };
 
@@ -760,18 +817,24 @@ bdk_status bdk_graph_create(bdk_cache* c, const bdk_attn_config* cfg, const void
   BDK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
   // the workspaces a step uses exist before capture (allocations do not
   // belong in a graph): one attend-only launch sizes them
-  const auto pb0 = c->packed_blocks, rl0 = c->res_len;
-  const uint64_t steps0 = c->fast_steps, launches0 = c->launches;
   s = run_decode_fast(c, cfg, q, nullptr, nullptr, out, nullptr, 0, 1 << 30, st, false);
   if (s == BDK_OK && cudaStreamSynchronize(st) != cudaSuccess)
     s = cuda_fail(cudaGetLastError(), "graph warm-up");
-  // capture: the host mirror advances as the steps are recorded (capacity
-  // checks run per step) and is restored afterwards -- the steps happen when
-  // the graph is launched
+  // two captures, one per parity of the first step (node i reads the len2
+  // half (p + i) & 1).  The host mirror advances as the steps are recorded
+  // (capacity checks run per step) and is restored afterwards -- the steps
+  // happen when the graph is launched
+  const auto pb0 = c->packed_blocks, rl0 = c->res_len;
+  const uint64_t steps0 = c->fast_steps, launches0 = c->launches;
   const size_t nq = (size_t)cfg->batch * cfg->heads_q * cfg->head_dim;
   const size_t nk = (size_t)cfg->batch * cfg->heads_kv * cfg->head_dim;
-  cudaGraph_t g = nullptr;
-  if (s == BDK_OK) {
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  for (int pass = 0; pass < 2 && s == BDK_OK; ++pass) {
+    c->packed_blocks = pb0;
+    c->res_len = rl0;
+    c->fast_steps = steps0 + pass;
+    point_lengths(c);
+    cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) s = cuda_fail(e, "cudaStreamBeginCapture");
     for (uint32_t i = 0; s == BDK_OK && i < n_steps; ++i) {
@@ -780,29 +843,34 @@ bdk_status bdk_graph_create(bdk_cache* c, const bdk_attn_config* cfg, const void
         s = run_decode_fast(c, cfg, static_cast<const __half*>(q) + i * nq,
                             static_cast<const __half*>(k_new) + i * nk,
                             static_cast<const __half*>(v_new) + i * nk, out + i * nq, nullptr, 0,
-                            1 << 30, st, false);
+                            1 << 30, st, false, /*dev_sched=*/true);
     }
     if (e == cudaSuccess) {
       const cudaError_t e2 = cudaStreamEndCapture(st, &g);
       if (s == BDK_OK && e2 != cudaSuccess) s = cuda_fail(e2, "cudaStreamEndCapture");
     }
+    if (s == BDK_OK) {
+      e = cudaGraphInstantiate(&exec[(steps0 + pass) & 1], g, 0);
+      if (e != cudaSuccess) s = cuda_fail(e, "cudaGraphInstantiate");
+    }
+    if (g) cudaGraphDestroy(g);
   }
   c->packed_blocks = pb0;
   c->res_len = rl0;
-  c->fast_steps = steps0 + (s == BDK_OK ? 1 : 0);  // the warm-up was a real (attend-only) step
-  c->launches = launches0 + (s == BDK_OK ? 1 : 0);
+  c->fast_steps = steps0;
+  c->launches = launches0;
+  c->blocks_written = true;
   point_lengths(c);
-  cudaGraphExec_t exec = nullptr;
-  if (s == BDK_OK) {
-    const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
-    if (e != cudaSuccess) s = cuda_fail(e, "cudaGraphInstantiate");
-  }
-  if (g) cudaGraphDestroy(g);
   cudaStreamDestroy(st);
-  if (s) return s;
+  if (s) {
+    for (auto& x : exec)
+      if (x) cudaGraphExecDestroy(x);
+    return s;
+  }
   auto* gr = new bdk_graph;
   gr->cache = c;
-  gr->exec = exec;
+  gr->exec[0] = exec[0];
+  gr->exec[1] = exec[1];
   gr->n_steps = n_steps;
   c->graphs += 1;
   *graph = gr;
@@ -810,7 +878,7 @@ bdk_status bdk_graph_create(bdk_cache* c, const bdk_attn_config* cfg, const void
 }
 
 bdk_status bdk_graph_launch(bdk_graph* gr, void* stream) {
-  if (!gr || !gr->exec) return fail(BDK_INVALID_ARGUMENT, "null graph");
+  if (!gr || !gr->exec[0] || !gr->exec[1]) return fail(BDK_INVALID_ARGUMENT, "null graph");
   bdk_cache* c = gr->cache;
   // capacity of the n_steps appends, on a copy of the mirror
   {
@@ -828,7 +896,7 @@ bdk_status bdk_graph_launch(bdk_graph* gr, void* stream) {
       }
   }
   DevGuard dev_guard_(c->device);
-  BDK_CUDA(cudaGraphLaunch(gr->exec, as_stream(stream)), "cudaGraphLaunch");
+  BDK_CUDA(cudaGraphLaunch(gr->exec[c->fast_steps & 1], as_stream(stream)), "cudaGraphLaunch");
   for (uint32_t i = 0; i < gr->n_steps; ++i) advance_fast_step(c, true);
   c->launches += gr->n_steps;
   return BDK_OK;
@@ -837,7 +905,8 @@ bdk_status bdk_graph_launch(bdk_graph* gr, void* stream) {
 bdk_status bdk_graph_destroy(bdk_graph* gr) {
   if (!gr) return BDK_OK;
   DevGuard dev_guard_(gr->cache->device);
-  if (gr->exec) cudaGraphExecDestroy(gr->exec);
+  for (auto& x : gr->exec)
+    if (x) cudaGraphExecDestroy(x);
   gr->cache->graphs -= 1;
   delete gr;
   return BDK_OK;
@@ -1327,6 +1396,7 @@ bdk_status bdk_build_block(bdk_cache* c, uint32_t b, uint32_t h, uint16_t* kw, u
   bdk_status s = check_cell(c, b, h);
   if (s) return s;
   const int i = cell_of(c, b, h);
+  c->blocks_written = true;  // packed records may change (no PDL prefetch next)
   if (c->res_len[i] != c->dev.G.n_r)
     return fail(BDK_STATE_ERROR, "build_block requires a full residual (res_len == N_r)");
   if (c->packed_blocks[i] >= c->dev.G.max_blocks)
@@ -1381,6 +1451,7 @@ bdk_status bdk_adopt_block(bdk_cache* c, uint32_t b, uint32_t h, const uint16_t*
   BDK_CUDA(cudaMemcpy(c->dev.packed_blocks + i, &nb, sizeof(int), cudaMemcpyHostToDevice),
            "H2D length");
   c->packed_blocks[i] = nb;
+  c->blocks_written = true;
   return BDK_OK;
 }
 
@@ -1440,6 +1511,7 @@ bdk_status bdk_corrupt_word(bdk_cache* c, uint32_t b, uint32_t h, uint32_t blk, 
                           word_offset(G, word),
                       &value, 2, cudaMemcpyHostToDevice),
            "H2D word");
+  c->blocks_written = true;
   return BDK_OK;
 }
 

@@ -1,9 +1,9 @@
 // bdk_decode_fast.cu -- the sm_100a decode hot kernel (fast mode).
 //
-// One launch performs decode_step's attention for every cell (attention.cpp:
-// 164-242): residual_attend + packed_attend + combine, with the append of the
-// new token fused in.  (The flush of a residual that became full runs as a
-// separate tiny launch, only on the steps where one fills.)
+// One launch performs decode_step for every cell (attention.cpp:164-242):
+// residual_attend + packed_attend + combine, with the append of the new token
+// fused in, and -- by the CTA that merges a cell -- the commit of its lengths
+// and the flush of a residual window the step filled (kvcache.cpp:208-237).
 //
 // Schedule -- stream-K over units.  Cell c (= b * heads_kv + h) owns
 // nb_c + 1 units: its packed blocks (in the attended range) and, last, its
@@ -42,6 +42,7 @@
 #include "bdk_frag.cuh"
 #include "bdk_launch.h"
 #include "bdk_qpack.cuh"
+#include "bdk_qpack_fast.cuh"
 
 namespace bdk {
 
@@ -99,38 +100,72 @@ __device__ __forceinline__ int cta_of_unit(long long u, long long T, int N) {
   return (int)(((u + 1) * (long long)N - 1) / T);
 }
 
-// The step's schedule, derived on the device from the cell lengths (so a step
-// is a fixed launch, capturable in a CUDA graph).  Cell c owns nb_c packed
-// blocks of the attended range then max(1, ceil(rlen_c / rt)) residual units
-// of rt tokens.  Lengths come from the half of the double buffer that no CTA
-// writes during this step (DevCache::len2); loads bypass L1.
+// The step's schedule.  Cell c owns nb_c packed blocks of the attended range
+// then max(1, ceil(rlen_c / rt)) residual units of rt tokens.  Lengths live in
+// the half of the double buffer that no CTA writes during this step
+// (DevCache::len2, FastArgs::par).  Host schedule (dev == 0): the unit counts
+// come from the launch arguments (uniform cells) or the uploaded prefix
+// arrays; device schedule (dev == 1, graph steps): from the lengths (L2 loads).
 struct Sched {
-  const int* pb;  // current packed block counts
-  const int* rl;  // current residual fills
-  int* pb_n;      // next step's lengths (merging CTAs write them)
-  int* rl_n;
-  int blk_begin, blk_end, rt, radd;  // radd: tokens this step appends (0/1), -1: no residual
+  // a view of the launch parameters (__grid_constant__: read from the
+  // constant bank on use, so nothing here occupies registers in the hot loop)
+  const DevCache* c;
+  const FastArgs* a;
+  int cells, rt;
+  __device__ __forceinline__ const int* pb() const { return c->len2 + (size_t)a->par * 2 * cells; }
+  __device__ __forceinline__ const int* rl() const { return pb() + cells; }
+  __device__ __forceinline__ int* pb_n() const { return c->len2 + (size_t)(a->par ^ 1) * 2 * cells; }
+  __device__ __forceinline__ int* rl_n() const { return pb_n() + cells; }
+  __device__ __forceinline__ int radd() const {
+    return a->skip_residual ? -1 : (a->k_new != nullptr ? 1 : 0);
+  }
   __device__ __forceinline__ int nb(int cell) const {
-    return max(0, min(blk_end, __ldcg(pb + cell)) - blk_begin);
+    if (!a->dev_sched) return a->uni_units ? a->uni_nb : __ldg(a->unit_nb + cell);
+    return max(0, min(a->blk_end, __ldcg(pb() + cell)) - a->blk_begin);
   }
   __device__ __forceinline__ int rlen(int cell) const {
-    return radd < 0 ? 0 : __ldcg(rl + cell) + radd;
+    return radd() < 0 ? 0 : __ldcg(rl() + cell) + radd();
   }
   __device__ __forceinline__ int units(int cell, int nbc) const {
+    if (!a->dev_sched)
+      return a->uni_units ? a->uni_units : __ldg(a->unit_off + cell + 1) - __ldg(a->unit_off + cell);
     return nbc + max(1, (rlen(cell) + rt - 1) / rt);
   }
 };
+
+__device__ __forceinline__ Sched make_sched(const DevCache& c, const FastArgs& a, int cells, int rt) {
+  return Sched{&c, &a, cells, rt};
+}
 
 struct SchedOut {
   long long T, off0;  // total units; first unit of cell0
   int cell0;
 };
-__device__ __forceinline__ int cell0_of(const SchedOut& so) { return so.cell0; }
 
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
+// host schedule: the cell holding unit u (largest c with unit_off[c] <= u)
+__device__ __forceinline__ int find_cell(const int* off, int cells, long long u) {
+  int lo = 0, hi = cells - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((long long)__ldg(off + mid) <= u)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ SchedOut sched_host(const Sched& S, const FastArgs& a, int cells) {
+  const long long T = a.total_units;
+  const long long neff = min((long long)gridDim.x, T);
+  const long long ub = (long long)blockIdx.x < neff ? (long long)blockIdx.x * T / neff : T;
+  if (ub >= T) return SchedOut{T, T, cells};
+  if (a.uni_units) {
+    const int c0 = (int)(ub / a.uni_units);
+    return SchedOut{T, (long long)c0 * a.uni_units, c0};
+  }
+  const int c0 = find_cell(a.unit_off, cells, ub);
+  return SchedOut{T, (long long)__ldg(a.unit_off + c0), c0};
 }
 
 // Block-wide scan of the cells' unit counts: total T and, for this CTA's
@@ -348,8 +383,16 @@ constexpr int MERGE_KC_FEW = 16;
 // per head, then every thread owns float4s of the output and issues the
 // chunk's loads back to back.  Measured faster than merge_cell below when a
 // cell has a handful of partials (C2: +2%), slower for tens (C5: -3%).
+// where a merge writes (passed by value: the merges are not inlined, and a
+// reference to the kernel's FastArgs would copy it to local memory)
+struct MergeDst {
+  float* out;
+  float* out_lse;
+  int heads_q, n_group;
+};
+
 template <int NC>
-__device__ void merge_cell_few(const FastArgs& a, const Geom& G, int cell, const float* base, int nk,
+__device__ void merge_cell_few(const MergeDst a, const Geom& G, int cell, const float* base, int nk,
                            float* sm, unsigned long long* tr) {
   constexpr int NTH = NC * 32;
   constexpr int NV = (8 * D / 4 + NTH - 1) / NTH;  // float4 outputs per thread (max)
@@ -464,7 +507,7 @@ __device__ __forceinline__ float4 merge_batch(const float4* po, int st4, const f
 }
 
 template <int NC>
-__device__ void merge_cell(const FastArgs& a, const Geom& G, int cell, const float* base, int nk,
+__device__ void merge_cell(const MergeDst a, const Geom& G, int cell, const float* base, int nk,
                            float* sm, unsigned long long* tr) {
   constexpr int NTH = NC * 32;
   constexpr int NV = (8 * D / 4 + NTH - 1) / NTH;  // float4 outputs per thread (max)
@@ -635,8 +678,7 @@ struct PrepCtx {
   int rec, prep_stride, pgrp;
   long long u_begin, u_end, off0;
   int cell0;
-  Sched S;
-  int redo, pf;  // full-barrier phase offset of the first pf stages (see full_par)
+  int rt;  // residual tokens per unit
 };
 
 // Prep warp: per packed block of its consumer group, fold the channel-wise K
@@ -646,7 +688,7 @@ struct PrepCtx {
 // of 4*NH channels), so only real heads cost work; Q' rows of heads >= n_group
 // stay zero (prep areas are zeroed at kernel start).
 template <int NH, int NS, int GRP>
-__device__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& px) {
+__device__ __forceinline__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& px) {
   constexpr int LPH = 32 / NH;  // lanes per head
   constexpr int CPL = D / LPH;  // channels per lane
   constexpr int H2 = CPL / 2;   // half2 per lane
@@ -654,11 +696,12 @@ __device__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& p
   const int lane = threadIdx.x & 31;
   const int h = lane % NH, cbk = lane / NH;
   const int ng = a.n_group;
+  const Sched S = make_sched(c, a, G.batch * G.heads_kv, px.rt);
   int it = 0;
   long long u = px.u_begin, off = px.off0;
   for (int cell = px.cell0; u < px.u_end; ++cell) {
-    const int nbc = px.S.nb(cell);
-    const long long ce = off + px.S.units(cell, nbc);
+    const int nbc = S.nb(cell);
+    const long long ce = off + S.units(cell, nbc);
     const long long seg_end = min(px.u_end, ce);
     const long long pk_end = min(seg_end, off + nbc);
     if (u < pk_end) {
@@ -683,7 +726,7 @@ __device__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& p
         if (GRP > 1 && (it % GRP) != px.pgrp) continue;
         const int s = it % NS;
         const unsigned long long tw = (px.tr && lane == 0) ? globaltimer() : 0ull;
-        mbar_wait_sleep(&px.full[s], ((it / NS) + ((px.redo && s < px.pf) ? 1 : 0)) & 1);
+        mbar_wait_sleep(&px.full[s], (it / NS) & 1);
         const unsigned long long tb = (px.tr && lane == 0) ? globaltimer() : 0ull;
         if (px.tr && lane == 0) px.tr[12] += tb - tw;
         if (!(a.dev_flags & 2)) {
@@ -961,7 +1004,7 @@ __device__ __forceinline__ void consume_residual(const DevCache& c, const FastAr
 
 template <int BITS, int WN, int NS, int MINB, int GRP, int CP>
 __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
-    decode_fast_kernel(DevCache c, FastArgs a) {
+    decode_fast_kernel(const __grid_constant__ DevCache c, const __grid_constant__ FastArgs a) {
   using C = FC<BITS, WN, MINB, GRP>;
   constexpr int P = C::P, NPAIR = C::NPAIR, NC = C::NC;
   static_assert(CP == 1 || (CP == 2 && NPAIR % 2 == 0), "column packing pairs tiles");
@@ -1006,87 +1049,20 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   // PDL: the next kernel may launch its CTAs as soon as every CTA of this one
   // is resident (the grid is one wave, so this cannot starve it)
   pdl_launch_dependents();
-  // ---- the step's schedule, from the device lengths.  Under PDL the
-  // previous step may still be committing them: read the step counter and
-  // its half of the lengths now (speculation), let the TMA warp stream the
-  // first records of that schedule, and verify after griddepcontrol.wait --
-  // the schedule stands unless the previous step changed some cell's unit
-  // count, which its merging CTAs flag per half (sched[2 + half]).
-  Sched S;
-  S.blk_begin = a.blk_begin;
-  S.blk_end = a.blk_end;
-  S.rt = 16 * NC;
-  S.radd = a.skip_residual ? -1 : (a.k_new != nullptr ? 1 : 0);
-  auto bind = [&](int step) {
-    const int par = step & 1;
-    S.pb = c.len2 + (size_t)par * 2 * cells;
-    S.rl = S.pb + cells;
-    S.pb_n = c.len2 + (size_t)(par ^ 1) * 2 * cells;
-    S.rl_n = S.pb_n + cells;
-  };
-  const int s0 = ld_acquire_gpu(c.sched);
-  bind(s0);
-  SchedOut so = sched_scan(S, cells, sched_sm);
-  long long T = so.T;
-  int N = (int)min((long long)gridDim.x, T);  // CTAs sharing the units
-  long long u_begin = (int)blockIdx.x < N ? (long long)blockIdx.x * T / N : T;
-  long long u_end = (int)blockIdx.x < N ? (long long)(blockIdx.x + 1) * T / N : T;
-  const uint64_t pol = policy_evict_first();
-  int pf = 0;  // records the TMA warp streamed on the speculative schedule
-  if (a.pdl && warp == NC && lane == 0) {
-    // only records at least two blocks behind a cell's newest one: older
-    // records are immutable whatever the previous step still writes
-    long long u = u_begin, off = so.off0;
-    for (int cell = cell0_of(so); u < u_end && pf < NS; ++cell) {
-      const int nbc = S.nb(cell);
-      const long long ce = off + S.units(cell, nbc);
-      const long long pk_end = min(min(u_end, ce), off + nbc);
-      const int pb_safe = __ldcg(S.pb + cell) - 2;
-      const uint8_t* base = c.records + (size_t)cell * G.max_blocks * REC;
-      for (long long x = u; x < pk_end && pf < NS; ++x) {
-        const int blk = a.blk_begin + (int)(x - off);
-        if (blk >= pb_safe) {
-          u = u_end;  // stop speculating (keeps the sequence a prefix)
-          break;
-        }
-        mbar_expect_tx(&full[pf], (uint32_t)REC);
-        tma_bulk_g2s(ring + (size_t)pf * REC, base + (size_t)blk * REC, (uint32_t)REC, &full[pf],
-                     pol);
-        ++pf;
-      }
-      if (u >= u_end) break;
-      u = min(u_end, ce);
-      off = ce;
-    }
-    sched_sm[14] = pf;
+  // ---- the step's schedule
+  const Sched S = make_sched(c, a, cells, 16 * NC);
+  SchedOut so;
+  if (a.dev_sched) {
+    // the lengths may still be being committed by the previous step
+    if (a.pdl) pdl_wait();
+    so = sched_scan(S, cells, sched_sm);
+  } else {
+    so = sched_host(S, a, cells);
   }
-  int redo = 0;
-  if (a.pdl) {
-    pdl_wait();
-    // every thread reads the same final words, so the outcome is CTA-uniform
-    // and the common (valid) path needs no barrier after the wait
-    const int s1 = __ldcg(c.sched);
-    const int ok = s1 == s0 || (s1 == s0 + 1 && __ldcg(c.sched + 2 + (s1 & 1)) == 0);
-    // the lengths this step reads and writes are always the final half; a
-    // valid speculation only means the unit counts (the schedule) agree
-    bind(s1);
-    if (!ok) {  // the previous step moved the schedule: rescan its lengths
-      redo = 1;
-      __syncthreads();  // publishes pf (TMA lane); sched_sm is reused by the scan
-      pf = (int)sched_sm[14];
-      so = sched_scan(S, cells, sched_sm);
-      T = so.T;
-      N = (int)min((long long)gridDim.x, T);
-      u_begin = (int)blockIdx.x < N ? (long long)blockIdx.x * T / N : T;
-      u_end = (int)blockIdx.x < N ? (long long)(blockIdx.x + 1) * T / N : T;
-    }
-  }
-  const int par_cur = (int)(S.pb - c.len2) / (2 * cells);
-  // full-barrier phase of ring iteration k at stage s: a stage that held a
-  // discarded speculative record completed one extra phase
-  auto full_par = [&](int k) -> uint32_t {
-    return (uint32_t)((k / NS) + ((redo && (k % NS) < pf) ? 1 : 0)) & 1u;
-  };
+  const long long T = so.T;
+  const int N = (int)min((long long)gridDim.x, T);  // CTAs sharing the units
+  const long long u_begin = (int)blockIdx.x < N ? (long long)blockIdx.x * T / N : T;
+  const long long u_end = (int)blockIdx.x < N ? (long long)(blockIdx.x + 1) * T / N : T;
   const int cell0 = so.cell0;
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * 16 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
@@ -1094,10 +1070,15 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   // ------------------------------------------------------------ TMA warp
   if (warp == NC) {
     if (lane == 0 && u_begin < u_end) {
-      // a rescheduled step discards the speculative records: let them land
-      // (their stages then complete one extra phase, see full_par)
-      if (redo)
-        for (int s = 0; s < pf; ++s) mbar_wait(&full[s], 0);
+      const uint64_t pol = policy_evict_first();
+      // the first NS records may stream in before the previous kernel ends
+      // when no packed record changed since (host schedule only: the records
+      // are immutable and the schedule is in the arguments)
+      bool waited = !a.pdl || a.dev_sched;
+      if (!a.prefetch_ok && !waited) {
+        pdl_wait();
+        waited = true;
+      }
       int it = 0;
       long long u = u_begin, off = so.off0;
       for (int cell = cell0; u < u_end; ++cell) {
@@ -1108,7 +1089,10 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
         const uint8_t* base = c.records + (size_t)cell * G.max_blocks * REC;
         for (long long x = u; x < pk_end; ++x, ++it) {
           const int s = it % NS;
-          if (!redo && it < pf) continue;  // streamed before griddepcontrol.wait
+          if (!waited && it == NS) {
+            pdl_wait();
+            waited = true;
+          }
           if (it >= NS) {
             const unsigned long long tw = tr ? globaltimer() : 0ull;
             mbar_wait_sleep(&empty[s], ((it / NS) - 1) & 1);
@@ -1125,6 +1109,8 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     }
     return;
   }
+  // q, lengths, counters and slots: after the previous kernel
+  if (a.pdl && !a.dev_sched) pdl_wait();
 
   // ---------------------------------------------------------- prep warps
   if (warp > NC) {
@@ -1132,7 +1118,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     const int pgrp = warp - NC - 1;  // prepares the blocks of consumer group pgrp
     const int nh = ng <= 1 ? 1 : ng <= 2 ? 2 : ng <= 4 ? 4 : 8;
     PrepCtx px{ring, prep, full, ready, tr, REC, (int)L.prep_stride, pgrp, u_begin, u_end,
-               so.off0, cell0, S, redo, pf};
+               so.off0, cell0, 16 * NC};
     if (nh == 1) prep_loop<1, NS, GRP>(c, a, px);
     else if (nh == 2) prep_loop<2, NS, GRP>(c, a, px);
     else if (nh == 4) prep_loop<4, NS, GRP>(c, a, px);
@@ -1184,7 +1170,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       unsigned long long tw = 0;
       if (tr && threadIdx.x == 0) tw = globaltimer();
       mbar_wait(&ready[s], (k / NS) & 1);
-      mbar_wait(&full[s], full_par(k));
+      mbar_wait(&full[s], (k / NS) & 1);
       if (tr && threadIdx.x == 0) {
         const unsigned long long now = globaltimer();
         if (k == 0) tr[1] = now; else tr[9] += now - tw;
@@ -1204,7 +1190,9 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     // ---------------- residual window (fp16), append fused.  Residual unit r
     // of a cell covers tokens [r*RT, (r+1)*RT) (RT = 16 per consumer warp);
     // the CTA whose range holds row res_len writes the new token there.
-    const int rl0 = __ldcg(S.rl + cell);
+    // the cell's lengths: from the arguments when the host schedule found
+    // them uniform, else from the current half
+    const int rl0 = a.uni_len ? a.uni_rl : __ldcg(S.rl() + cell);
     const bool app = a.k_new != nullptr && !a.skip_residual;
     float oscale_seg = oscale;
     if (seg_end > res_begin && !a.skip_residual) {
@@ -1248,30 +1236,29 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     if (commit) {
       const float* base = a.slots + (size_t)(lo + cell) * stride_slot;
       if (hi - lo + 1 <= MERGE_KC_FEW)
-        merge_cell_few<NC>(a, G, cell, base, hi - lo + 1, merge_sm, tr);
+        merge_cell_few<NC>(MergeDst{a.out, a.out_lse, a.heads_q, a.n_group}, G, cell, base, hi - lo + 1, merge_sm, tr);
       else
-        merge_cell<NC>(a, G, cell, base, hi - lo + 1, merge_sm, tr);
-      const int pb0 = __ldcg(S.pb + cell);
+        merge_cell<NC>(MergeDst{a.out, a.out_lse, a.heads_q, a.n_group}, G, cell, base, hi - lo + 1, merge_sm, tr);
+      const int pb0 = a.uni_len ? a.uni_pb : __ldcg(S.pb() + cell);
       if (commit == 2) {
         // build_block + commit_block (kvcache.cpp:208-237) after the step's
         // attention (attention.cpp:235-240): quantize + pack the full window
         // into the cell's next block slot
         named_bar(1, NC * 32);
         const size_t wo = (size_t)cell * G.n_r * D;
-        flush_window<BITS>(G, c.res_k + wo, c.res_v + wo,
-                           c.records + ((size_t)cell * G.max_blocks + pb0) * REC, NC * 32, 1);
+        uint8_t* rec = c.records + ((size_t)cell * G.max_blocks + pb0) * REC;
+        // N_r = 8 * WN * P: a multiple of 128 takes the tile path of the
+        // qpack_fast geometry (fast_decode_ok: d = g = 128, KChannel K)
+        if constexpr ((NC == 2 || NC == 4 || NC == 8) && BITS != 8 && (WN * P) % 16 == 0) {
+          qf_flush_window<BITS, NC * 32>(G, c.res_k + wo, c.res_v + wo, rec,
+                                         reinterpret_cast<uint8_t*>(merge_sm), 1);
+        } else {
+          flush_window<BITS>(G, c.res_k + wo, c.res_v + wo, rec, NC * 32, 1);
+        }
       }
       if (threadIdx.x == 0) {
-        const int pbn = commit == 2 ? pb0 + 1 : pb0;
-        const int rln = commit == 2 ? 0 : rl0 + (app ? 1 : 0);
-        S.pb_n[cell] = pbn;
-        S.rl_n[cell] = rln;
-        // does the next launch (appending or not) see a different unit count
-        // for this cell?  Then a speculative schedule read from this step's
-        // half is stale (the flag of the half just written)
-        auto nres = [&](int r) { return max(1, (r + S.rt - 1) / S.rt); };
-        if (pbn != pb0 || nres(rln) != nres(rl0) || nres(rln + 1) != nres(rl0 + 1))
-          atomicOr(c.sched + 2 + (par_cur ^ 1), 1);
+        S.pb_n()[cell] = commit == 2 ? pb0 + 1 : pb0;
+        S.rl_n()[cell] = commit == 2 ? 0 : rl0 + (app ? 1 : 0);
       }
     }
     if (tr && threadIdx.x == 0) {
@@ -1288,17 +1275,6 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     named_bar(1, NC * 32);  // flag / merge smem reuse by the next segment
     u = seg_end;
     off = ce;
-  }
-  // ---- step end: the last CTA to finish bumps the step, so the next launch
-  // reads the lengths this one's merging CTAs wrote (every cell has a merge)
-  if (threadIdx.x == 0) {
-    const int prev = atom_add_acq_rel_gpu(c.sched + 1, 1);
-    if (prev == (int)gridDim.x - 1) {
-      c.sched[1] = 0;
-      c.sched[2 + par_cur] = 0;  // the half the next step writes starts unflagged
-      __threadfence();           // lengths + flags before the step (speculative readers)
-      c.sched[0] = c.sched[0] + 1;
-    }
   }
 }
 

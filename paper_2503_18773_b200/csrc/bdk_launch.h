@@ -20,12 +20,10 @@ struct DevCache {
   int* packed_blocks = nullptr;  // [cells]
   int* res_len = nullptr;        // [cells]
   // double-buffered lengths of the fast decode: [2][packed_blocks | res_len][cells].
-  // A fast step reads half (step & 1) and its merging CTAs write every cell's
-  // next lengths into the other half; the last CTA to exit bumps the step.
-  // So the schedule is read from memory nothing writes during the step, and
-  // a step is a fixed launch (capturable in a CUDA graph).
+  // Fast step s reads half (s & 1) -- FastArgs::par, from the host's step
+  // count -- and its merging CTAs write every cell's next lengths into the
+  // other half, so nothing a step reads changes while it runs.
   int* len2 = nullptr;
-  int* sched = nullptr;  // [0] step (fast decode launches), [1] CTAs exited this step
 };
 
 struct DecodeArgs {
@@ -60,10 +58,25 @@ struct FastArgs {
   int n_ctas = 0, heads_q = 0, n_group = 0;
   int blk_begin = 0, blk_end = 1 << 30;  // packed block range attended
   int skip_residual = 0;  // residual units attend nothing (sequence-split ranks)
+  int par = 0;            // half of DevCache::len2 this step reads (step & 1)
+  // schedule.  dev_sched = 0: from the host mirror of the lengths -- every
+  // cell uni_units units of which uni_nb packed, or (uni_units == 0) the
+  // uploaded prefix unit_off [cells + 1] and unit_nb [cells]; total_units.
+  // dev_sched = 1: scanned on the device from len2 (a launch whose arguments
+  // hold for any lengths: the steps of a captured CUDA graph)
+  int dev_sched = 0;
+  long long total_units = 0;
+  int uni_units = 0, uni_nb = 0;
+  int uni_len = 0, uni_pb = 0, uni_rl = 0;  // host schedule: every cell has these lengths
+  const int* unit_off = nullptr;
+  const int* unit_nb = nullptr;
   float sm_scale_log2 = 0.f;
   unsigned long long* trace = nullptr;  // dev: [n_ctas][16] globaltimer stamps
   int dev_flags = 0;                    // dev probes (BDK_DEV_FLAGS): 1 no compute, 2 no prep
   int pdl = 0;  // launched as a programmatic dependent of the previous kernel
+  int prefetch_ok = 0;  // no packed record changed since the previous kernel: the
+                        // TMA warp may stream the first ring stages before
+                        // griddepcontrol.wait
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
 };
 

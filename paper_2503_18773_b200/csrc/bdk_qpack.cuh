@@ -220,8 +220,10 @@ __device__ inline void qpack_block(const Geom& G, const __half* k, const __half*
 // reduces its row per warp with the first-zero sign rule; codes are packed
 // straight into the swizzled word rows (thread per channel row), the V
 // params read back from the record the first pass wrote.
+// (G by value: the callers' geometry is a kernel parameter, whose address
+// would make them keep it in local memory)
 template <int BITS>
-__device__ __noinline__ void flush_window(const Geom& G, const __half* rk, const __half* rv,
+__device__ __noinline__ void flush_window(const Geom G, const __half* rk, const __half* rv,
                                     uint8_t* rec, int nthr, int bar) {
   constexpr int P = 16 / BITS;
   const float qmax = static_cast<float>((1u << BITS) - 1u);

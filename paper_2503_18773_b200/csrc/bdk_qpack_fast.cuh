@@ -82,14 +82,15 @@ __device__ __noinline__ uint32_t exact_word(const __half* tile, const float4* fs
 // is one 128-token group).  Codes need no clamp here: z = lo exactly and
 // s >= (hi - lo) / qmax * (1 - 2^-11), so every in-group quotient lies in
 // [0, qmax + 0.5).
-template <int BITS, bool TOKEN_PARAMS, bool IL>
+// (NT: threads [0, NT) of the CTA take part; `tile` may be shared or global)
+template <int BITS, bool TOKEN_PARAMS, bool IL, int NT = QF_THREADS>
 __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, uint8_t* words,
                                         const Geom& G, int hf) {
   constexpr int P = 16 / BITS;
   constexpr int CPT = QF_D / (8 * P);  // 16-byte chunks per row in one tile
   // SPLIT threads share a chunk (4 / SPLIT word pairs each) so that all
-  // QF_THREADS threads have an item at 2-bit too
-  constexpr int SPLIT = QF_THREADS / (CPT * (QF_D / 2)) < 1 ? 1 : QF_THREADS / (CPT * (QF_D / 2));
+  // NT threads have an item at 2-bit too
+  constexpr int SPLIT = NT / (CPT * (QF_D / 2)) < 1 ? 1 : NT / (CPT * (QF_D / 2));
   constexpr int NP = 4 / SPLIT;  // u32 word pairs per item
   const __half2* tile2 = reinterpret_cast<const __half2*>(tile);
   const int wn = G.warp_n, rb = 16 * wn;
@@ -110,7 +111,8 @@ __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, ui
   uint32_t bias = 0;
 #pragma unroll
   for (int p = 0; p < P; ++p) bias += MAGIC_BITS << (p * BITS);
-  for (int item = threadIdx.x; item < SPLIT * CPT * (QF_D / 2); item += QF_THREADS) {
+  static_assert((SPLIT * CPT * (QF_D / 2)) % NT == 0, "every lane of a warp has an item");
+  for (int item = threadIdx.x; item < SPLIT * CPT * (QF_D / 2); item += NT) {
     const int sp = item / (CPT * (QF_D / 2));
     const int jl = (item / (QF_D / 2)) % CPT, cp = item % (QF_D / 2);
     const int t0 = jl * 8 * P + sp * NP * 2 * P;  // first token (tile-relative)
@@ -320,6 +322,114 @@ __global__ void __launch_bounds__(QF_THREADS) qpack_fast_kernel(DevCache c, cons
       qf_pack<BITS, true, false>(tile, fs, rec + G.wbytes, G, hf);
   }
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
+// Fused flush of one full residual window (build_block + commit_block,
+// kvcache.cpp:208-237) inside the fast decode kernel, by its NT consumer
+// threads (named barrier `bar`), for the qpack_fast geometry.  Same
+// arithmetic as qpack_fast_kernel -- bit-exact with the reference -- but the
+// 128-token tiles are read straight from the (L2-resident) window instead of
+// being staged: the ring of the merging CTA may already hold its next cell's
+// blocks.  `sm` >= 3 KB of shared scratch: fs (128 float4) + K partial
+// (lo, hi) half2 per (part, channel pair).
+template <int BITS, int NT>
+__device__ __forceinline__ void qf_flush_window(const Geom& G, const __half* rk, const __half* rv,
+                                                uint8_t* rec, uint8_t* sm, int bar) {
+  static_assert(NT >= 64 && NT % 64 == 0, "channel pairs x token parts");
+  constexpr int PARTS = NT / 64, TPP = QF_D / PARTS;  // K scan: token parts, tokens per part
+  const float qmax = static_cast<float>((1u << BITS) - 1u);
+  float4* fs = reinterpret_cast<float4*>(sm);
+  __half2* plo = reinterpret_cast<__half2*>(sm + QF_D * 16);
+  __half2* phi = plo + PARTS * 64;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* kp = reinterpret_cast<uint32_t*>(rec + 2 * G.wbytes);
+  uint32_t* vp = reinterpret_cast<uint32_t*>(rec + 2 * G.wbytes + G.kp_bytes);
+  for (int hf = 0; hf < G.n_r / QF_D; ++hf) {
+    // ---- K: KChannel group = the tile's 128 tokens of one channel
+    const __half* kt = rk + (size_t)hf * QF_D * QF_D;
+    const __half2* kt2 = reinterpret_cast<const __half2*>(kt);
+    {
+      const int cp = tid % 64, part = tid / 64;
+      const int t0 = part * TPP;
+      __half2 lo = kt2[(size_t)t0 * 64 + cp], hi = lo;
+#pragma unroll 16
+      for (int t = t0 + 1; t < t0 + TPP; ++t) {
+        const __half2 x = kt2[(size_t)t * 64 + cp];
+        lo = __hmin2(lo, x);
+        hi = __hmax2(hi, x);
+      }
+      plo[part * 64 + cp] = lo;
+      phi[part * 64 + cp] = hi;
+    }
+    named_bar(bar, NT);
+    for (int ch = tid; ch < QF_D; ch += NT) {
+      float lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+      for (int p = 0; p < PARTS; ++p) {
+        const __half2 l2 = plo[p * 64 + ch / 2], h2 = phi[p * 64 + ch / 2];
+        lo = fminf(lo, __half2float((ch & 1) ? __high2half(l2) : __low2half(l2)));
+        hi = fmaxf(hi, __half2float((ch & 1) ? __high2half(h2) : __low2half(h2)));
+      }
+      if (lo == 0.f || hi == 0.f) {  // sign of the first zero in token order
+        for (int t = 0; t < QF_D; ++t) {
+          const float x = __half2float(kt[(size_t)t * QF_D + ch]);
+          if (x == 0.f) {
+            if (lo == 0.f) lo = x;
+            if (hi == 0.f) hi = x;
+            break;
+          }
+        }
+      }
+      float s, z;
+      group_params(lo, hi, qmax, s, z);
+      fs[ch] = make_float4(s, z, __frcp_rn(s), 0.f);
+      kp[hf * QF_D + ch] = param_u32(s, z);
+    }
+    named_bar(bar, NT);
+    if (G.interleave)
+      qf_pack<BITS, false, true, NT>(kt, fs, rec, G, hf);
+    else
+      qf_pack<BITS, false, false, NT>(kt, fs, rec, G, hf);
+    named_bar(bar, NT);  // fs is reused
+    // ---- V: token groups (the 128 channels of one token); warp per token
+    const __half* vt = rv + (size_t)hf * QF_D * QF_D;
+    const __half2* vt2 = reinterpret_cast<const __half2*>(vt);
+    for (int t = warp; t < QF_D; t += NT / 32) {
+      const __half2 a = vt2[(size_t)t * 64 + lane], b = vt2[(size_t)t * 64 + 32 + lane];
+      const __half2 lo2 = __hmin2(a, b), hi2 = __hmax2(a, b);
+      float lo = fminf(__low2float(lo2), __high2float(lo2));
+      float hi = fmaxf(__low2float(hi2), __high2float(hi2));
+      // first zero in channel order (channels 2*lane, 2*lane+1, 64+2*lane, ...)
+      int zf = 0x7fffffff;
+      if (__low2float(a) == 0.f) zf = 2 * lane;
+      else if (__high2float(a) == 0.f) zf = 2 * lane + 1;
+      else if (__low2float(b) == 0.f) zf = 64 + 2 * lane;
+      else if (__high2float(b) == 0.f) zf = 65 + 2 * lane;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        zf = min(zf, __shfl_xor_sync(0xffffffffu, zf, o));
+      }
+      if (lo == 0.f || hi == 0.f) {
+        const float x = __half2float(vt[(size_t)t * QF_D + zf]);
+        if (lo == 0.f) lo = x;
+        if (hi == 0.f) hi = x;
+      }
+      if (lane == 0) {
+        float s, z;
+        group_params(lo, hi, qmax, s, z);
+        fs[t] = make_float4(s, z, __frcp_rn(s), 0.f);
+        vp[hf * QF_D + t] = param_u32(s, z);
+      }
+    }
+    named_bar(bar, NT);
+    if (G.interleave)
+      qf_pack<BITS, true, true, NT>(vt, fs, rec + G.wbytes, G, hf);
+    else
+      qf_pack<BITS, true, false, NT>(vt, fs, rec + G.wbytes, G, hf);
+    named_bar(bar, NT);
+  }
 }
 
 }  // namespace bdk
