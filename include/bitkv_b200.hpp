@@ -411,32 +411,48 @@ class PagePool {
   PagePool(size_t page_size, size_t head_dim, size_t max_pages = 0)
       : page_size_(page_size), head_dim_(head_dim), max_pages_(max_pages) {}
 
-  // a recycled page first (most recently released), else a new one;
-  // CapacityError once max_pages pages exist and none is free
+  // Pages live in one growing slab ([k rows | v rows] per page).  Released
+  // handles form an intrusive LIFO list threaded through next_free_, so the
+  // most recently released page is handed out first (the reference's
+  // recycling order, kvcache.hpp:50-52).
   uint32_t alloc() {
-    if (!free_.empty()) {
-      const uint32_t id = free_.back();
-      free_.pop_back();
+    if (head_ != kNone) {
+      const uint32_t id = head_;
+      head_ = next_free_[id];
+      next_free_[id] = kLive;
+      --n_free_;
       return id;
     }
-    if (max_pages_ && k_.size() >= max_pages_) throw CapacityError("page pool exhausted");
-    k_.emplace_back(page_size_ * head_dim_, 0.0f);
-    v_.emplace_back(page_size_ * head_dim_, 0.0f);
-    return static_cast<uint32_t>(k_.size() - 1);
+    const size_t n = next_free_.size();
+    if (max_pages_ != 0 && n == max_pages_) throw CapacityError("PagePool: all pages in use");
+    slab_.resize(slab_.size() + 2 * page_floats(), 0.0f);
+    next_free_.push_back(kLive);
+    return static_cast<uint32_t>(n);
   }
-  void release(uint32_t id) { free_.push_back(id); }
+  void release(uint32_t id) {
+    next_free_[id] = head_;
+    head_ = id;
+    ++n_free_;
+  }
 
-  float* k_row(uint32_t page, size_t slot) { return k_[page].data() + slot * head_dim_; }
-  float* v_row(uint32_t page, size_t slot) { return v_[page].data() + slot * head_dim_; }
-  const float* k_row(uint32_t page, size_t slot) const { return k_[page].data() + slot * head_dim_; }
-  const float* v_row(uint32_t page, size_t slot) const { return v_[page].data() + slot * head_dim_; }
+  float* k_row(uint32_t page, size_t slot) { return slab_.data() + row_off(page, slot, 0); }
+  float* v_row(uint32_t page, size_t slot) { return slab_.data() + row_off(page, slot, 1); }
+  const float* k_row(uint32_t page, size_t slot) const { return slab_.data() + row_off(page, slot, 0); }
+  const float* v_row(uint32_t page, size_t slot) const { return slab_.data() + row_off(page, slot, 1); }
 
   size_t page_size() const { return page_size_; }
-  size_t live_pages() const { return k_.size() - free_.size(); }
+  size_t live_pages() const { return next_free_.size() - n_free_; }
 
  private:
-  std::vector<std::vector<float>> k_, v_;
-  std::vector<uint32_t> free_;
+  static constexpr uint32_t kNone = 0xFFFFFFFFu, kLive = 0xFFFFFFFEu;
+  size_t page_floats() const { return page_size_ * head_dim_; }
+  size_t row_off(uint32_t page, size_t slot, int half) const {
+    return (2 * (size_t)page + (size_t)half) * page_floats() + slot * head_dim_;
+  }
+  std::vector<float> slab_;
+  std::vector<uint32_t> next_free_;  // per page: next released page, or kLive
+  uint32_t head_ = kNone;
+  size_t n_free_ = 0;
   size_t page_size_ = 0, head_dim_ = 0, max_pages_ = 0;
 };
 
@@ -448,30 +464,39 @@ struct PageTable {  // logical tokens -> pool pages; pages == ceil(length / page
 
 inline void paged_append(PageTable& pt, PagePool& pool, const float* k_row, const float* v_row,
                          size_t d) {
-  const size_t slot = pt.length % pt.page_size;
-  if (slot == 0) pt.pages.push_back(pool.alloc());
-  std::memcpy(pool.k_row(pt.pages.back(), slot), k_row, d * sizeof(float));
-  std::memcpy(pool.v_row(pt.pages.back(), slot), v_row, d * sizeof(float));
-  ++pt.length;
+  if (pt.pages.size() * pt.page_size == pt.length) pt.pages.push_back(pool.alloc());  // last page full
+  const uint32_t page = pt.pages.back();
+  const size_t slot = pt.length - (pt.pages.size() - 1) * pt.page_size;
+  std::copy(k_row, k_row + d, pool.k_row(page, slot));
+  std::copy(v_row, v_row + d, pool.v_row(page, slot));
+  pt.length += 1;
 }
 
+// tokens [t0, t0 + len) page run by page run (rows of a page are contiguous)
 inline void paged_gather(const PageTable& pt, const PagePool& pool, size_t t0, size_t len,
                          size_t d, float* k_out, float* v_out) {
-  if (t0 + len > pt.length) throw ShapeError("paged_gather: range past end of table");
-  for (size_t i = 0; i < len; ++i) {
-    const size_t t = t0 + i;
+  if (len > pt.length || t0 > pt.length - len)
+    throw ShapeError("paged_gather: tokens [t0, t0 + len) exceed the table");
+  size_t done = 0;
+  while (done < len) {
+    const size_t t = t0 + done;
+    const size_t slot = t % pt.page_size;
+    const size_t run = std::min(len - done, pt.page_size - slot);
     const uint32_t page = pt.pages[t / pt.page_size];
-    std::memcpy(k_out + i * d, pool.k_row(page, t % pt.page_size), d * sizeof(float));
-    std::memcpy(v_out + i * d, pool.v_row(page, t % pt.page_size), d * sizeof(float));
+    std::copy(pool.k_row(page, slot), pool.k_row(page, slot) + run * d, k_out + done * d);
+    std::copy(pool.v_row(page, slot), pool.v_row(page, slot) + run * d, v_out + done * d);
+    done += run;
   }
 }
 
 inline void paged_pop_front(PageTable& pt, PagePool& pool, size_t n_tokens) {
-  if (n_tokens > pt.length) throw StateError("paged_pop_front: more tokens than resident");
-  if (n_tokens % pt.page_size != 0) throw StateError("paged_pop_front: must drop whole pages");
-  const size_t n = n_tokens / pt.page_size;
-  for (size_t i = 0; i < n; ++i) pool.release(pt.pages[i]);
-  pt.pages.erase(pt.pages.begin(), pt.pages.begin() + static_cast<std::ptrdiff_t>(n));
+  if (n_tokens > pt.length) throw StateError("paged_pop_front: fewer tokens resident");
+  const size_t whole = n_tokens / pt.page_size;
+  if (whole * pt.page_size != n_tokens) throw StateError("paged_pop_front: partial page");
+  std::for_each(pt.pages.begin(), pt.pages.begin() + static_cast<std::ptrdiff_t>(whole),
+                [&pool](uint32_t id) { pool.release(id); });
+  std::rotate(pt.pages.begin(), pt.pages.begin() + static_cast<std::ptrdiff_t>(whole), pt.pages.end());
+  pt.pages.resize(pt.pages.size() - whole);
   pt.length -= n_tokens;
 }
 

@@ -26,10 +26,11 @@ print("merge (last CTAs)", q((a[m, 5] - a[m, 4]) / 1e3), "n=", m.sum())
 if a.shape[1] > 10 and (a[m, 10] > 0).all():
     print("  of which atomic ", q((a[m, 10] - a[m, 4]) / 1e3))
     print("  merge_cell      ", q((a[m, 5] - a[m, 10]) / 1e3))
-    if (a[m, 14] > 0).all():  # merge_cell stamps (merge_cell_few has none)
-        print("    ml loads      ", q((a[m, 14] - a[m, 10]) / 1e3))
-        print("    weights+o     ", q((a[m, 15] - a[m, 14]) / 1e3))
-        print("    rest          ", q((a[m, 5] - a[m, 15]) / 1e3))
+    m2 = m & (a[:, 14] > 0) & (a[:, 15] > 0)  # merge_cell stamps (merge_cell_few has none)
+    if m2.any():
+        print("    ml loads      ", q((a[m2, 14] - a[m2, 10]) / 1e3), "n=", m2.sum())
+        print("    weights+o     ", q((a[m2, 15] - a[m2, 14]) / 1e3))
+        print("    rest          ", q((a[m2, 5] - a[m2, 15]) / 1e3))
     print("  merge end (abs) ", q((a[m, 5] - t0) / 1e3))
     print("  loop end of last", q((a[m, 2] - t0) / 1e3))
 print("units/CTA", q(a[:, 7]))
