@@ -506,7 +506,7 @@ __device__ __forceinline__ float4 merge_batch(const float4* po, int st4, const f
   return s4;
 }
 
-template <int NC>
+template <int NC, int LB = MERGE_LB>
 __device__ void merge_cell(const MergeDst a, const Geom& G, int cell, const float* base, int nk,
                            float* sm, unsigned long long* tr) {
   constexpr int NTH = NC * 32;
@@ -584,8 +584,8 @@ __device__ void merge_cell(const MergeDst a, const Geom& G, int cell, const floa
         if (kc <= 8 * ngrp)
           s4 = merge_batch<8>(po, st4, wk, h, grp, ngrp, kc, s4);
         else
-          for (int kb = grp; kb < kc; kb += MERGE_LB * ngrp)
-            s4 = merge_batch<MERGE_LB>(po, st4, wk, h, kb, ngrp, kc, s4);
+          for (int kb = grp; kb < kc; kb += LB * ngrp)
+            s4 = merge_batch<LB>(po, st4, wk, h, kb, ngrp, kc, s4);
         acc[v] = s4;
       }
     }
@@ -1278,6 +1278,8 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   }
 }
 
+#include "bdk_decode_split.cuh"
+
 }  // namespace
 
 bool fast_decode_ok(const Geom& G, int n_group) {
@@ -1297,7 +1299,22 @@ bool fast_decode_ok(const Geom& G, int n_group) {
 struct Variant {
   const void* fn;
   int ns, grp;
+  int split = 0;  // decode_split_kernel (QK / PV warp pairs)
 };
+
+template <int BITS, int WN, int NS>
+static Variant split_variant() {
+  return Variant{reinterpret_cast<const void*>(decode_split_kernel<BITS, WN, NS>), NS, 1, 1};
+}
+
+// dev knob BDK_SPLIT: 1 = split consumers for the 2/4-bit W_n = 4 kernels
+static int split_knob() {
+  static int v = [] {
+    const char* e = getenv("BDK_SPLIT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
 
 template <int BITS, int WN, int NS, int MINB, int GRP>
 static Variant variant(int cp) {
@@ -1331,6 +1348,10 @@ static Variant fast_kernel(const Geom& G, int ng) {
                                 : col_pack(G, ng);
 #define BDK_SEL(B, W, NS, MB, GR) \
   if (G.bits == B && G.warp_n == W) return variant<B, W, NS, MB, GR>(cp);
+  if (split_knob() == 1) {
+    if (G.bits == 2 && G.warp_n == 4) return split_variant<2, 4, 3>();
+    if (G.bits == 4 && G.warp_n == 4) return split_variant<4, 4, 4>();
+  }
   if (v == 2) {
     BDK_SEL(2, 4, 8, 1, 2) BDK_SEL(4, 4, 8, 1, 2)
   } else if (v == 3) {
@@ -1343,19 +1364,25 @@ static Variant fast_kernel(const Geom& G, int ng) {
   return Variant{nullptr, 0, 1};
 }
 
-static int fast_threads(const Geom& G, int grp) { return (G.warp_n * grp + 1 + grp) * 32; }
+static int fast_threads(const Geom& G, const Variant& k) {
+  return k.split ? (2 * G.warp_n + 2) * 32 : (G.warp_n * k.grp + 1 + k.grp) * 32;
+}
+
+static uint32_t fast_smem(const Geom& G, int ng, const Variant& k) {
+  return k.split ? split_layout(G, ng, k.ns, G.warp_n).total : smem_layout(G, ng, k.ns, k.grp).total;
+}
 
 int fast_residual_tokens(const Geom& G) { return 16 * G.warp_n * fast_kernel(G, 1).grp; }
 
 int fast_decode_ctas_per_sm(const Geom& G, int n_group) {
   const Variant k = fast_kernel(G, n_group);
   if (!k.fn) return 0;
-  const Smem L = smem_layout(G, n_group, k.ns, k.grp);
-  if (cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) !=
+  const uint32_t smem = fast_smem(G, n_group, k);
+  if (cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return 0;
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k.fn, fast_threads(G, k.grp), L.total) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k.fn, fast_threads(G, k), smem) !=
       cudaSuccess)
     return 0;
   return n;
@@ -1364,15 +1391,15 @@ int fast_decode_ctas_per_sm(const Geom& G, int n_group) {
 cudaError_t launch_decode_fast(const DevCache& c, const FastArgs& a, cudaStream_t s) {
   const Variant k = fast_kernel(c.G, a.n_group);
   if (!k.fn) return cudaErrorInvalidValue;
-  const Smem L = smem_layout(c.G, a.n_group, k.ns, k.grp);
+  const uint32_t smem = fast_smem(c.G, a.n_group, k);
   DevCache cc = c;
   FastArgs aa = a;
   void* args[] = {&cc, &aa};
   if (a.ev_begin) cudaEventRecord(a.ev_begin, s);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.n_ctas);
-  cfg.blockDim = dim3(fast_threads(c.G, k.grp));
-  cfg.dynamicSmemBytes = L.total;
+  cfg.blockDim = dim3(fast_threads(c.G, k));
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
