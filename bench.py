@@ -492,14 +492,15 @@ def run_decode(args, name, mode, world, rank, local, steps, warmup, e2e_steps, s
         return None
     gbs = total_bytes / (ms * 1e-3) / 1e9
     peak, peak_src = peak_hbm()
-    # steady state: one attention launch per step, back to back (PDL-overlapped)
+    # steady state: one step = the attention grid + its combine grid, back to
+    # back (programmatic dependent launch overlaps each with its predecessor)
     per_launch_bytes = bytes_total / K
     step_ms = ms / K
     achieved = per_launch_bytes / (step_ms * 1e-3) / 1e9
     kern_avg_ms = kern_ms / max(launches, 1)
     iso = per_launch_bytes / (kern_avg_ms * 1e-3) / 1e9 if launches else None
-    kern_name = ("bdk::decode_fast_kernel (stream-K attention over packed blocks + residual + "
-                 "in-kernel LSE merge)" if mode == "fast" else
+    kern_name = ("bdk::decode_fast_kernel (stream-K attention over packed blocks + residual) + "
+                 "bdk::combine_fast_kernel (LSE merge, commit, fused flush)" if mode == "fast" else
                  "bdk::decode_kernel + combine (bit-faithful dequant, hi/lo split PV)")
     res = {
         "metric": METRIC, "value": round(gbs, 1), "unit": "GB/s", "n_gpus": world, "steps": K,

@@ -153,9 +153,11 @@ BDK_API bdk_status bdk_decode_step(bdk_cache* cache, const bdk_attn_config* cfg,
  * attention.cpp:164-242, Algorithm 2's steady-state loop): step i reads
  * q_dev + i*batch*heads_q*d, k_new_dev/v_new_dev + i*batch*heads_kv*d
  * (binary16) and writes out_dev + i*batch*heads_q*d (fp32).  Every step is
- * ONE launch -- append, attention, combine and the flush of a residual
- * window that fills (build_block + commit_block, kvcache.cpp:208-237) --
- * scheduled on the device from the cache's device lengths, so one captured
+ * a fixed pair of launches -- the attention grid (append, residual and
+ * packed attention) and its combine grid (LSE merge, length commit and the
+ * flush of a residual window that fills, build_block + commit_block,
+ * kvcache.cpp:208-237) -- scheduled on the device from the cache's device
+ * lengths, so one captured
  * graph replays correctly at any cache state, flush steps included, and
  * bit-identically to the same steps run eagerly.  Fast mode only
  * (bdk_set_precise(cache, 0); else BDK_UNSUPPORTED).  Each launch checks the

@@ -50,7 +50,6 @@ struct bdk_cache {
   int* unit_off = nullptr;            // device host-schedule [unit_off (cells + 1) | unit_nb (cells)]
   std::vector<int> unit_off_host;     // last uploaded host schedule
   bool blocks_written = true;         // a packed record may have changed since the last fast step
-  int* counters = nullptr;            // device [cells]
   int graphs = 0;                     // live bdk_graph objects (workspaces are pinned)
   float* slots = nullptr;             // device partial slots
   size_t slot_floats = 0;
@@ -272,10 +271,6 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
       return fail(BDK_CUDA_ERROR, "fast decode kernel does not fit on this device");
   }
   const int n_ctas = c->fast_ctas_per_sm * c->num_sms;  // one wave, every step
-  if (!c->counters) {
-    BDK_CUDA(cudaMalloc(&c->counters, cells * sizeof(int)), "cudaMalloc(counters)");
-    BDK_CUDA(cudaMemsetAsync(c->counters, 0, cells * sizeof(int), stream), "cudaMemset(counters)");
-  }
   const size_t need = (size_t)(n_ctas + cells) * bdk::slot_stride(ng);
   if (need > c->slot_floats) {
     if (c->graphs > 0)
@@ -295,7 +290,6 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
   a.out = out;
   a.out_lse = lse;
   a.slots = c->slots;
-  a.counters = c->counters;
   a.n_ctas = n_ctas;
   a.heads_q = static_cast<int>(cfg->heads_q);
   a.n_group = ng;
@@ -364,7 +358,7 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
     a.trace = trace;
   }
   BDK_CUDA(bdk::launch_decode_fast(c->dev, a, stream), "fast decode launch");
-  c->launches += 1;
+  c->launches += 2;  // attention grid + combine grid
   if (trace) {
     std::vector<unsigned long long> h((size_t)n_ctas * 16);
     BDK_CUDA(cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, stream),
@@ -639,7 +633,6 @@ bdk_status bdk_cache_destroy(bdk_cache* c) {
   cudaFree(c->part_o);
   cudaFree(c->part_ml);
   cudaFree(c->span_parts);
-  cudaFree(c->counters);
   cudaFree(c->slots);
   for (auto& ev : c->events) {
     cudaEventDestroy(ev.first);
@@ -898,7 +891,7 @@ bdk_status bdk_graph_launch(bdk_graph* gr, void* stream) {
   DevGuard dev_guard_(c->device);
   BDK_CUDA(cudaGraphLaunch(gr->exec[c->fast_steps & 1], as_stream(stream)), "cudaGraphLaunch");
   for (uint32_t i = 0; i < gr->n_steps; ++i) advance_fast_step(c, true);
-  c->launches += gr->n_steps;
+  c->launches += 2 * (uint64_t)gr->n_steps;
   return BDK_OK;
 }
 

@@ -1,9 +1,12 @@
 // bdk_decode_fast.cu -- the sm_100a decode hot kernel (fast mode).
 //
-// One launch performs decode_step for every cell (attention.cpp:164-242):
-// residual_attend + packed_attend + combine, with the append of the new token
-// fused in, and -- by the CTA that merges a cell -- the commit of its lengths
-// and the flush of a residual window the step filled (kvcache.cpp:208-237).
+// A step of decode_step for every cell (attention.cpp:164-242) is two grids:
+//   decode_fast_kernel   residual_attend + packed_attend as stream-K
+//                        partials, with the append of the new token fused in;
+//   combine_fast_kernel  combine (the LSE merge of each cell's partials), the
+//                        commit of the cell's lengths and the flush of a
+//                        residual window the step filled (kvcache.cpp:
+//                        208-237); a programmatic dependent of the first.
 //
 // Schedule -- stream-K over units.  Cell c (= b * heads_kv + h) owns
 // nb_c + 1 units: its packed blocks (in the attended range) and, last, its
@@ -12,9 +15,8 @@
 // SM streams the same number of blocks whatever the batch / context shape
 // (b=1 128K and b=32 8K alike).  A CTA range may span several cells; each
 // (CTA, cell) segment leaves one partial (unnormalized O, running max, sum)
-// in slot i + c (injective), and the CTA that completes a cell (atomic
-// counter) LSE-merges its partials into the output (combine,
-// attention.cpp:142-162).
+// in slot i + c (injective); the combine grid merges the slots of cell c,
+// those of CTAs cta_of_unit(first unit of c) .. cta_of_unit(last unit of c).
 //
 // CTA = WN consumer warps + 1 TMA warp + 1 prep warp:
 //   TMA warp   one lane streams whole block records (K words | V words |
@@ -367,259 +369,6 @@ __device__ __forceinline__ void finalize_segment(Soft st, float (&o)[OT][4], flo
     }
   }
   named_bar(1, NC * 32);
-}
-
-// LSE merge of all partials of `cell` (combine, attention.cpp:142-162).
-// It runs on the kernel's tail, on the critical path of the step, so it is
-// written for latency: per chunk of up to MERGE_KC contributors, (1) every
-// (max, sum) pair is fetched in ONE round into shared memory, (2) each warp
-// turns the pairs of some heads into weights (lanes over contributors,
-// shuffle reductions), (3) each thread owns one float4 of the output in one
-// contributor group and issues MERGE_LB of its loads back to back.
-constexpr int MERGE_KC_FEW = 16;
-
-// LSE merge for few contributors (<= MERGE_KC_FEW, the batched-decode case):
-// one round of (max, sum) loads into shared memory, weights by one thread
-// per head, then every thread owns float4s of the output and issues the
-// chunk's loads back to back.  Measured faster than merge_cell below when a
-// cell has a handful of partials (C2: +2%), slower for tens (C5: -3%).
-// where a merge writes (passed by value: the merges are not inlined, and a
-// reference to the kernel's FastArgs would copy it to local memory)
-struct MergeDst {
-  float* out;
-  float* out_lse;
-  int heads_q, n_group;
-};
-
-template <int NC>
-__device__ void merge_cell_few(const MergeDst a, const Geom& G, int cell, const float* base, int nk,
-                           float* sm, unsigned long long* tr) {
-  constexpr int NTH = NC * 32;
-  constexpr int NV = (8 * D / 4 + NTH - 1) / NTH;  // float4 outputs per thread (max)
-  const int ng = a.n_group;
-  const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
-  const int stride = slot_stride(ng);
-  float* msh = sm;        // [8] running max per head
-  float* lsh = sm + 8;    // [8] running sum per head
-  float* rsh = sm + 16;   // [8] rescale of the previous chunks
-  float* wk = sm + 24;    // [MERGE_KC_FEW][8] weights
-  float* lk = wk + MERGE_KC_FEW * 8;  // [MERGE_KC_FEW][8] sums
-  const int nvec = ng * D / 4;
-  float4 acc[NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (threadIdx.x < 8) {
-    msh[threadIdx.x] = -INFINITY;
-    lsh[threadIdx.x] = 0.f;
-  }
-  for (int k0 = 0; k0 < nk; k0 += MERGE_KC_FEW) {
-    const int kc = min(MERGE_KC_FEW, nk - k0);
-    for (int idx = threadIdx.x; idx < kc * ng; idx += NTH) {
-      const int k = idx / ng, h = idx % ng;
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(
-          base + (size_t)(k0 + k) * stride + ng * D + 2 * h));
-      wk[k * 8 + h] = ml.x;
-      lk[k * 8 + h] = ml.y;
-    }
-    named_bar(1, NTH);
-    if (threadIdx.x < ng) {
-      const int h = threadIdx.x;
-      const float mo = msh[h];
-      float mx = mo;
-      for (int k = 0; k < kc; ++k) mx = fmaxf(mx, wk[k * 8 + h]);
-      const float r = mo == -INFINITY ? 0.f : ex2(mo - mx);
-      float l = lsh[h] * r;
-      for (int k = 0; k < kc; ++k) {
-        const float m = wk[k * 8 + h];
-        const float w = m == -INFINITY ? 0.f : ex2(m - mx);
-        wk[k * 8 + h] = w;
-        l = fmaf(lk[k * 8 + h], w, l);
-      }
-      lsh[h] = l;
-      msh[h] = mx;
-      rsh[h] = r;
-    }
-    named_bar(1, NTH);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const int e = threadIdx.x + v * NTH;
-      if (e < nvec) {
-        const int h = (4 * e) / D;
-        const float r = rsh[h];
-        float4 s4 = make_float4(acc[v].x * r, acc[v].y * r, acc[v].z * r, acc[v].w * r);
-        const float4* po = reinterpret_cast<const float4*>(base + (size_t)k0 * stride) + e;
-        const int st4 = stride / 4;
-        float4 o[MERGE_KC_FEW];
-#pragma unroll
-        for (int k = 0; k < MERGE_KC_FEW; ++k)
-          o[k] = k < kc ? __ldcg(po + (size_t)k * st4) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < MERGE_KC_FEW; ++k) {
-          const float w = k < kc ? wk[k * 8 + h] : 0.f;
-          s4.x = fmaf(o[k].x, w, s4.x);
-          s4.y = fmaf(o[k].y, w, s4.y);
-          s4.z = fmaf(o[k].z, w, s4.z);
-          s4.w = fmaf(o[k].w, w, s4.w);
-        }
-        acc[v] = s4;
-      }
-    }
-    named_bar(1, NTH);  // wk / lk reused by the next chunk
-  }
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    const int e = threadIdx.x + v * NTH;
-    if (e < nvec) {
-      const int h = (4 * e) / D, ch = (4 * e) % D;
-      const float l = lsh[h];
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      const size_t row = (size_t)bidx * a.heads_q + (size_t)hk * ng + h;
-      const float4 s4 = acc[v];
-      *reinterpret_cast<float4*>(a.out + row * D + ch) =
-          make_float4(s4.x * inv, s4.y * inv, s4.z * inv, s4.w * inv);
-      if (a.out_lse != nullptr && ch == 0)
-        a.out_lse[row] = l > 0.f ? msh[h] + __log2f(l) : -INFINITY;
-    }
-  }
-}
-
-// s4 += sum over contributors k = kb, kb + step, ... (LB of them, < kc) of
-// w_k * o_k, all LB loads issued back to back
-template <int LB>
-__device__ __forceinline__ float4 merge_batch(const float4* po, int st4, const float* wk, int h,
-                                              int kb, int step, int kc, float4 s4) {
-  float4 o[LB];
-#pragma unroll
-  for (int i = 0; i < LB; ++i) {
-    const int k = kb + i * step;
-    o[i] = k < kc ? __ldcg(po + (size_t)k * st4) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-#pragma unroll
-  for (int i = 0; i < LB; ++i) {
-    const int k = kb + i * step;
-    const float w = k < kc ? wk[k * 8 + h] : 0.f;
-    s4.x = fmaf(o[i].x, w, s4.x);
-    s4.y = fmaf(o[i].y, w, s4.y);
-    s4.z = fmaf(o[i].z, w, s4.z);
-    s4.w = fmaf(o[i].w, w, s4.w);
-  }
-  return s4;
-}
-
-template <int NC, int LB = MERGE_LB>
-__device__ void merge_cell(const MergeDst a, const Geom& G, int cell, const float* base, int nk,
-                           float* sm, unsigned long long* tr) {
-  constexpr int NTH = NC * 32;
-  constexpr int NV = (8 * D / 4 + NTH - 1) / NTH;  // float4 outputs per thread (max)
-  const int ng = a.n_group;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
-  const int stride = slot_stride(ng);
-  const int st4 = stride / 4;
-  (void)cell;
-  float* msh = sm;        // [8] running max per head
-  float* lsh = sm + 8;    // [8] running sum per head
-  float* rsh = sm + 16;   // [8] rescale of the previous chunks
-  float* wk = sm + 24;    // [MERGE_KC][8] weights
-  float* lk = wk + MERGE_KC * 8;                           // [MERGE_KC][8] sums
-  float4* red = reinterpret_cast<float4*>(lk + MERGE_KC * 8);  // [NTH] group reduction
-  const int nvec = ng * D / 4;
-  // n_group <= NTH*4/D: one float4 per thread, the spare threads split the
-  // contributors into groups; else NV float4 per thread, one group
-  const bool grouped = nvec <= NTH;
-  const int ngrp = grouped ? NTH / nvec : 1;
-  const int grp = grouped ? threadIdx.x / nvec : 0;
-  float4 acc[NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (threadIdx.x < 8) {
-    msh[threadIdx.x] = -INFINITY;
-    lsh[threadIdx.x] = 0.f;
-  }
-  for (int k0 = 0; k0 < nk; k0 += MERGE_KC) {
-    const int kc = min(MERGE_KC, nk - k0);
-    for (int idx = threadIdx.x; idx < kc * ng; idx += NTH) {
-      const int k = idx / ng, h = idx % ng;
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(
-          base + (size_t)(k0 + k) * stride + ng * D + 2 * h));
-      wk[k * 8 + h] = ml.x;
-      lk[k * 8 + h] = ml.y;
-    }
-    named_bar(1, NTH);
-    if (tr && threadIdx.x == 0 && k0 == 0) tr[14] = globaltimer();
-    for (int h = warp; h < ng; h += NC) {
-      float mx = -INFINITY;
-      for (int k = lane; k < kc; k += 32) mx = fmaxf(mx, wk[k * 8 + h]);
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      const float mo = msh[h];
-      const float mn = fmaxf(mo, mx);
-      float l = 0.f;
-      for (int k = lane; k < kc; k += 32) {
-        const float m = wk[k * 8 + h];
-        const float w = m == -INFINITY ? 0.f : ex2(m - mn);
-        wk[k * 8 + h] = w;
-        l = fmaf(lk[k * 8 + h], w, l);
-      }
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-      __syncwarp();
-      if (lane == 0) {
-        const float r = mo == -INFINITY ? 0.f : ex2(mo - mn);
-        lsh[h] = fmaf(lsh[h], r, l);
-        msh[h] = mn;
-        rsh[h] = r;
-      }
-    }
-    named_bar(1, NTH);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const int e = grouped ? (v == 0 ? threadIdx.x % nvec : nvec) : threadIdx.x + v * NTH;
-      if (e < nvec && grp < ngrp) {
-        const int h = (4 * e) / D;
-        const float r = rsh[h];
-        float4 s4 = make_float4(acc[v].x * r, acc[v].y * r, acc[v].z * r, acc[v].w * r);
-        const float4* po = reinterpret_cast<const float4*>(base + (size_t)k0 * stride) + e;
-        // few contributors (the usual case): a short batch; else deep batches
-        if (kc <= 8 * ngrp)
-          s4 = merge_batch<8>(po, st4, wk, h, grp, ngrp, kc, s4);
-        else
-          for (int kb = grp; kb < kc; kb += LB * ngrp)
-            s4 = merge_batch<LB>(po, st4, wk, h, kb, ngrp, kc, s4);
-        acc[v] = s4;
-      }
-    }
-    named_bar(1, NTH);  // wk / lk reused by the next chunk
-    if (tr && threadIdx.x == 0 && k0 == 0) tr[15] = globaltimer();
-  }
-  if (ngrp > 1) {  // sum the contributor groups
-    red[threadIdx.x] = acc[0];
-    named_bar(1, NTH);
-    if (threadIdx.x < nvec) {
-      for (int g = 1; g < ngrp; ++g) {
-        const float4 x = red[g * nvec + threadIdx.x];
-        acc[0].x += x.x;
-        acc[0].y += x.y;
-        acc[0].z += x.z;
-        acc[0].w += x.w;
-      }
-    }
-  }
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    const int e = threadIdx.x + v * NTH;
-    if (e < nvec) {
-      const int h = (4 * e) / D, ch = (4 * e) % D;
-      const float l = lsh[h];
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      const size_t row = (size_t)bidx * a.heads_q + (size_t)hk * ng + h;
-      const float4 s4 = acc[v];
-      *reinterpret_cast<float4*>(a.out + row * D + ch) =
-          make_float4(s4.x * inv, s4.y * inv, s4.z * inv, s4.w * inv);
-      if (a.out_lse != nullptr && ch == 0)
-        a.out_lse[row] = l > 0.f ? msh[h] + __log2f(l) : -INFINITY;
-    }
-  }
 }
 
 // Fold of one staged block for the prep warp: Q'[h][c] = fp16(q[h][c] s_c)
@@ -1218,52 +967,9 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     float* slot = a.slots + (size_t)(blockIdx.x + cell) * stride_slot;
     finalize_segment<NC, CP>(st, o, merge_sm, ng, slot, oscale_seg);  // ends with a barrier
     if (tr && threadIdx.x == 0) tr[4] = globaltimer();
-    const int lo = cta_of_unit(cb, T, N), hi = cta_of_unit(ce - 1, T, N);
-    if (threadIdx.x == 0) {
-      // release the slot writes of all consumer threads (ordered before this
-      // thread by the barrier) and acquire the other contributors' slots
-      const int prev = atom_add_acq_rel_gpu(a.counters + cell, 1);
-      const int last = prev == hi - lo;
-      if (last) a.counters[cell] = 0;
-      // the step's commit of this cell (merging CTA, after every contributor
-      // has read the window): 1 = lengths carried over (+ the append),
-      // 2 = the append filled the window -> flush it into a new block
-      flag[0] = !last ? 0 : (app && rl0 + 1 == G.n_r) ? 2 : 1;
-    }
-    named_bar(1, NC * 32);
-    if (tr && threadIdx.x == 0) tr[10] = globaltimer();
-    const int commit = flag[0];
-    if (commit) {
-      const float* base = a.slots + (size_t)(lo + cell) * stride_slot;
-      if (hi - lo + 1 <= MERGE_KC_FEW)
-        merge_cell_few<NC>(MergeDst{a.out, a.out_lse, a.heads_q, a.n_group}, G, cell, base, hi - lo + 1, merge_sm, tr);
-      else
-        merge_cell<NC>(MergeDst{a.out, a.out_lse, a.heads_q, a.n_group}, G, cell, base, hi - lo + 1, merge_sm, tr);
-      const int pb0 = a.uni_len ? a.uni_pb : __ldcg(S.pb() + cell);
-      if (commit == 2) {
-        // build_block + commit_block (kvcache.cpp:208-237) after the step's
-        // attention (attention.cpp:235-240): quantize + pack the full window
-        // into the cell's next block slot
-        named_bar(1, NC * 32);
-        const size_t wo = (size_t)cell * G.n_r * D;
-        uint8_t* rec = c.records + ((size_t)cell * G.max_blocks + pb0) * REC;
-        // N_r = 8 * WN * P: a multiple of 128 takes the tile path of the
-        // qpack_fast geometry (fast_decode_ok: d = g = 128, KChannel K)
-        if constexpr ((NC == 2 || NC == 4 || NC == 8) && BITS != 8 && (WN * P) % 16 == 0) {
-          qf_flush_window<BITS, NC * 32>(G, c.res_k + wo, c.res_v + wo, rec,
-                                         reinterpret_cast<uint8_t*>(merge_sm), 1);
-        } else {
-          flush_window<BITS>(G, c.res_k + wo, c.res_v + wo, rec, NC * 32, 1);
-        }
-      }
-      if (threadIdx.x == 0) {
-        S.pb_n()[cell] = commit == 2 ? pb0 + 1 : pb0;
-        S.rl_n()[cell] = commit == 2 ? 0 : rl0 + (app ? 1 : 0);
-      }
-    }
     if (tr && threadIdx.x == 0) {
       tr[5] = globaltimer();
-      tr[6] = (unsigned long long)(commit != 0);
+      tr[6] = 0;
       tr[7] = (unsigned long long)(u_end - u_begin);
       unsigned int smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -1272,13 +978,145 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     // every consumer warp has left its claim loop: restart the claims at the
     // next cell's first block
     if (GRP > 1 && threadIdx.x < WN) claim[threadIdx.x] = it;
-    named_bar(1, NC * 32);  // flag / merge smem reuse by the next segment
+    named_bar(1, NC * 32);  // merge smem reuse by the next segment
     u = seg_end;
     off = ce;
   }
 }
 
-#include "bdk_decode_split.cuh"
+// ---------------------------------------------------------------------------
+// combine (attention.cpp:142-162) + the step's commit (kvcache.cpp:170-251).
+// A separate small grid chained to the attention grid by programmatic
+// dependent launch: CTA (cell, h) LSE-merges the cell's partial slots for
+// query head h of the group (thread = channel; every (max, sum) pair and O
+// value of a batch of contributors in flight at once), so the merge runs on
+// cells x n_group CTAs in parallel instead of on the tail of the CTA that
+// finished a cell last.  CTA (cell, 0) then commits the cell's next lengths
+// into the other half of len2 and, when the step filled the residual window,
+// quantizes + packs it into the cell's next block slot (the fused flush).
+constexpr int CMB_LB = 48;  // contributors per load batch (one round for C1-C5)
+
+template <int BITS, int WN>
+__global__ void __launch_bounds__(D) combine_fast_kernel(const __grid_constant__ DevCache c,
+                                                         const __grid_constant__ FastArgs a) {
+  __shared__ __align__(16) uint8_t sm[4096];
+  pdl_launch_dependents();  // the next step's prologue and prefetch may start
+  const Geom& G = c.G;
+  const int cells = G.batch * G.heads_kv;
+  const int cell = blockIdx.x, h = blockIdx.y, ch = threadIdx.x;
+  const int ng = a.n_group;
+  const Sched S = make_sched(c, a, cells, a.rt);
+  if (a.pdl) pdl_wait();  // the attention grid's partials (and, dev schedule, its lengths)
+  // the cell's unit range [cb, ce) and total T: host schedule from the
+  // arguments, device schedule by a block reduction over the lengths
+  long long cb, ce, T;
+  if (!a.dev_sched) {
+    T = a.total_units;
+    if (a.uni_units) {
+      cb = (long long)cell * a.uni_units;
+      ce = cb + a.uni_units;
+    } else {
+      cb = __ldg(a.unit_off + cell);
+      ce = __ldg(a.unit_off + cell + 1);
+    }
+  } else {
+    long long* red = reinterpret_cast<long long*>(sm);
+    long long before = 0, all = 0, mine = 0;
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) {
+      const long long u = S.units(i, S.nb(i));
+      all += u;
+      if (i < cell) before += u;
+      if (i == cell) mine = u;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      before += __shfl_xor_sync(0xffffffffu, before, o);
+      all += __shfl_xor_sync(0xffffffffu, all, o);
+      mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    }
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+      red[warp] = before;
+      red[8 + warp] = all;
+      red[16 + warp] = mine;
+    }
+    __syncthreads();
+    before = all = mine = 0;
+    for (int w = 0; w < nw; ++w) {
+      before += red[w];
+      all += red[8 + w];
+      mine += red[16 + w];
+    }
+    __syncthreads();
+    cb = before;
+    ce = before + mine;
+    T = all;
+  }
+  const int N = (int)min((long long)a.n_ctas, T);
+  const int lo = cta_of_unit(cb, T, N), hi = cta_of_unit(ce - 1, T, N);
+  const int nk = hi - lo + 1;
+  const int stride = slot_stride(ng);
+  const float* base = a.slots + (size_t)(lo + cell) * stride;
+  // online LSE merge over the contributors, CMB_LB loads of each kind in flight
+  float M = -INFINITY, L = 0.f, acc = 0.f;
+  for (int k0 = 0; k0 < nk; k0 += CMB_LB) {
+    float mk[CMB_LB], lk[CMB_LB], ok[CMB_LB];
+#pragma unroll
+    for (int i = 0; i < CMB_LB; ++i) {
+      const int k = k0 + i;
+      if (k < nk) {
+        const float* sl = base + (size_t)k * stride;
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(sl + ng * D + 2 * h));
+        mk[i] = ml.x;
+        lk[i] = ml.y;
+        ok[i] = __ldcg(sl + h * D + ch);
+      } else {
+        mk[i] = -INFINITY;
+        lk[i] = 0.f;
+        ok[i] = 0.f;
+      }
+    }
+    float mx = M;
+#pragma unroll
+    for (int i = 0; i < CMB_LB; ++i) mx = fmaxf(mx, mk[i]);
+    const float r = M == -INFINITY ? 0.f : ex2(M - mx);
+    acc *= r;
+    L *= r;
+#pragma unroll
+    for (int i = 0; i < CMB_LB; ++i) {
+      const float w = mk[i] == -INFINITY ? 0.f : ex2(mk[i] - mx);
+      acc = fmaf(ok[i], w, acc);
+      L = fmaf(lk[i], w, L);
+    }
+    M = mx;
+  }
+  const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
+  const size_t row = (size_t)bidx * a.heads_q + (size_t)hk * ng + h;
+  a.out[row * D + ch] = L > 0.f ? acc / L : 0.f;
+  if (a.out_lse != nullptr && ch == 0) a.out_lse[row] = L > 0.f ? M + __log2f(L) : -INFINITY;
+  if (h != 0) return;
+  // ---- the step's commit of this cell (every contributor has read the window)
+  const bool app = a.k_new != nullptr && !a.skip_residual;
+  const int rl0 = a.uni_len ? a.uni_rl : __ldcg(S.rl() + cell);
+  const int pb0 = a.uni_len ? a.uni_pb : __ldcg(S.pb() + cell);
+  const bool fill = app && rl0 + 1 == G.n_r;
+  if (fill) {
+    // build_block + commit_block (kvcache.cpp:208-237) after the step's
+    // attention (attention.cpp:235-240)
+    constexpr int P = 16 / BITS;
+    const size_t wo = (size_t)cell * G.n_r * D;
+    uint8_t* rec = c.records + ((size_t)cell * G.max_blocks + pb0) * G.rec_bytes;
+    if constexpr (BITS != 8 && (WN * P) % 16 == 0) {
+      qf_flush_window<BITS, D>(G, c.res_k + wo, c.res_v + wo, rec, sm, 1);
+    } else {
+      flush_window<BITS>(G, c.res_k + wo, c.res_v + wo, rec, D, 1);
+    }
+  }
+  if (threadIdx.x == 0) {
+    S.pb_n()[cell] = fill ? pb0 + 1 : pb0;
+    S.rl_n()[cell] = fill ? 0 : rl0 + (app ? 1 : 0);
+  }
+}
 
 }  // namespace
 
@@ -1299,32 +1137,19 @@ bool fast_decode_ok(const Geom& G, int n_group) {
 struct Variant {
   const void* fn;
   int ns, grp;
-  int split = 0;  // decode_split_kernel (QK / PV warp pairs)
+  const void* combine;  // combine_fast_kernel of the same geometry
 };
-
-template <int BITS, int WN, int NS>
-static Variant split_variant() {
-  return Variant{reinterpret_cast<const void*>(decode_split_kernel<BITS, WN, NS>), NS, 1, 1};
-}
-
-// dev knob BDK_SPLIT: 1 = split consumers for the 2/4-bit W_n = 4 kernels
-static int split_knob() {
-  static int v = [] {
-    const char* e = getenv("BDK_SPLIT");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
 
 template <int BITS, int WN, int NS, int MINB, int GRP>
 static Variant variant(int cp) {
+  const void* comb = reinterpret_cast<const void*>(combine_fast_kernel<BITS, WN>);
   if constexpr (BITS != 8) {
     if (cp == 2)
       return Variant{reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP, 2>),
-                     NS, GRP};
+                     NS, GRP, comb};
   }
   return Variant{reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP, 1>), NS,
-                 GRP};
+                 GRP, comb};
 }
 
 static int variant_knob() {
@@ -1348,10 +1173,6 @@ static Variant fast_kernel(const Geom& G, int ng) {
                                 : col_pack(G, ng);
 #define BDK_SEL(B, W, NS, MB, GR) \
   if (G.bits == B && G.warp_n == W) return variant<B, W, NS, MB, GR>(cp);
-  if (split_knob() == 1) {
-    if (G.bits == 2 && G.warp_n == 4) return split_variant<2, 4, 3>();
-    if (G.bits == 4 && G.warp_n == 4) return split_variant<4, 4, 4>();
-  }
   if (v == 2) {
     BDK_SEL(2, 4, 8, 1, 2) BDK_SEL(4, 4, 8, 1, 2)
   } else if (v == 3) {
@@ -1361,15 +1182,15 @@ static Variant fast_kernel(const Geom& G, int ng) {
   BDK_SEL(4, 1, 4, 2, 1) BDK_SEL(4, 2, 4, 2, 1) BDK_SEL(4, 4, 4, 2, 1) BDK_SEL(4, 8, 4, 1, 1)
   BDK_SEL(8, 1, 4, 2, 1) BDK_SEL(8, 2, 4, 2, 1) BDK_SEL(8, 4, 4, 2, 1) BDK_SEL(8, 8, 4, 1, 1)
 #undef BDK_SEL
-  return Variant{nullptr, 0, 1};
+  return Variant{nullptr, 0, 1, nullptr};
 }
 
 static int fast_threads(const Geom& G, const Variant& k) {
-  return k.split ? (2 * G.warp_n + 2) * 32 : (G.warp_n * k.grp + 1 + k.grp) * 32;
+  return (G.warp_n * k.grp + 1 + k.grp) * 32;
 }
 
 static uint32_t fast_smem(const Geom& G, int ng, const Variant& k) {
-  return k.split ? split_layout(G, ng, k.ns, G.warp_n).total : smem_layout(G, ng, k.ns, k.grp).total;
+  return smem_layout(G, ng, k.ns, k.grp).total;
 }
 
 int fast_residual_tokens(const Geom& G) { return 16 * G.warp_n * fast_kernel(G, 1).grp; }
@@ -1394,19 +1215,31 @@ cudaError_t launch_decode_fast(const DevCache& c, const FastArgs& a, cudaStream_
   const uint32_t smem = fast_smem(c.G, a.n_group, k);
   DevCache cc = c;
   FastArgs aa = a;
+  aa.rt = 16 * c.G.warp_n * k.grp;
   void* args[] = {&cc, &aa};
   if (a.ev_begin) cudaEventRecord(a.ev_begin, s);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.n_ctas);
   cfg.blockDim = dim3(fast_threads(c.G, k));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelExC(&cfg, k.fn, args);
+  if (e != cudaSuccess) return e;
+  // combine: one CTA per (cell, query head of the group), a programmatic
+  // dependent of the attention grid (it waits for the partials itself)
+  cudaLaunchConfig_t cfg2 = {};
+  cfg2.gridDim = dim3(c.G.batch * c.G.heads_kv, a.n_group);
+  cfg2.blockDim = dim3(D);
+  cfg2.dynamicSmemBytes = 0;
+  cfg2.stream = s;
+  cfg2.attrs = attr;
+  cfg2.numAttrs = 1;
+  e = cudaLaunchKernelExC(&cfg2, k.combine, args);
   if (e != cudaSuccess) return e;
   if (a.ev_end) cudaEventRecord(a.ev_end, s);
   return cudaSuccess;

@@ -54,11 +54,11 @@ struct FastArgs {
   float* out = nullptr;      // [batch][heads_q][d]
   float* out_lse = nullptr;  // optional [batch][heads_q] (log2 domain)
   float* slots = nullptr;    // [n_ctas + cells][n_group][d + 2] partials
-  int* counters = nullptr;   // [cells], zero between launches
   int n_ctas = 0, heads_q = 0, n_group = 0;
   int blk_begin = 0, blk_end = 1 << 30;  // packed block range attended
   int skip_residual = 0;  // residual units attend nothing (sequence-split ranks)
   int par = 0;            // half of DevCache::len2 this step reads (step & 1)
+  int rt = 0;             // residual tokens per unit (set by launch_decode_fast)
   // schedule.  dev_sched = 0: from the host mirror of the lengths -- every
   // cell uni_units units of which uni_nb packed, or (uni_units == 0) the
   // uploaded prefix unit_off [cells + 1] and unit_nb [cells]; total_units.
