@@ -1094,7 +1094,6 @@ __global__ void __launch_bounds__(D) combine_fast_kernel(const __grid_constant__
   const size_t row = (size_t)bidx * a.heads_q + (size_t)hk * ng + h;
   a.out[row * D + ch] = L > 0.f ? acc / L : 0.f;
   if (a.out_lse != nullptr && ch == 0) a.out_lse[row] = L > 0.f ? M + __log2f(L) : -INFINITY;
-  if (h != 0) return;
   // ---- the step's commit of this cell (every contributor has read the window)
   const bool app = a.k_new != nullptr && !a.skip_residual;
   const int rl0 = a.uni_len ? a.uni_rl : __ldcg(S.rl() + cell);
@@ -1102,16 +1101,18 @@ __global__ void __launch_bounds__(D) combine_fast_kernel(const __grid_constant__
   const bool fill = app && rl0 + 1 == G.n_r;
   if (fill) {
     // build_block + commit_block (kvcache.cpp:208-237) after the step's
-    // attention (attention.cpp:235-240)
+    // attention (attention.cpp:235-240); the cell's n_group CTAs split the
+    // window's K and V tiles
     constexpr int P = 16 / BITS;
     const size_t wo = (size_t)cell * G.n_r * D;
     uint8_t* rec = c.records + ((size_t)cell * G.max_blocks + pb0) * G.rec_bytes;
     if constexpr (BITS != 8 && (WN * P) % 16 == 0) {
-      qf_flush_window<BITS, D>(G, c.res_k + wo, c.res_v + wo, rec, sm, 1);
-    } else {
+      qf_flush_window<BITS, D>(G, c.res_k + wo, c.res_v + wo, rec, sm, 1, h, ng);
+    } else if (h == 0) {
       flush_window<BITS>(G, c.res_k + wo, c.res_v + wo, rec, D, 1);
     }
   }
+  if (h != 0) return;
   if (threadIdx.x == 0) {
     S.pb_n()[cell] = fill ? pb0 + 1 : pb0;
     S.rl_n()[cell] = fill ? 0 : rl0 + (app ? 1 : 0);

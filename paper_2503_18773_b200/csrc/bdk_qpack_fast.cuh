@@ -325,18 +325,21 @@ __global__ void __launch_bounds__(QF_THREADS) qpack_fast_kernel(DevCache c, cons
 }
 
 // Fused flush of one full residual window (build_block + commit_block,
-// kvcache.cpp:208-237) inside the fast decode kernel, by its NT consumer
-// threads (named barrier `bar`), for the qpack_fast geometry.  Same
+// kvcache.cpp:208-237) by the combine grid: threads [0, NT) of a CTA pack the
+// window's tiles item0, item0 + istep, ... (item i < N_r/128: K tile i, else
+// V tile i - N_r/128), so the CTAs of one cell split the window.  Same
 // arithmetic as qpack_fast_kernel -- bit-exact with the reference -- but the
 // 128-token tiles are read straight from the (L2-resident) window instead of
-// being staged: the ring of the merging CTA may already hold its next cell's
-// blocks.  `sm` >= 3 KB of shared scratch: fs (128 float4) + K partial
-// (lo, hi) half2 per (part, channel pair).
+// being staged.  `sm` >= 3 KB of shared scratch: fs (128 float4) + K partial
+// (lo, hi) half2 per (part, channel pair).  Synchronized by named barrier
+// `bar` over NT threads.
 template <int BITS, int NT>
 __device__ __forceinline__ void qf_flush_window(const Geom& G, const __half* rk, const __half* rv,
-                                                uint8_t* rec, uint8_t* sm, int bar) {
+                                                uint8_t* rec, uint8_t* sm, int bar, int item0,
+                                                int istep) {
   static_assert(NT >= 64 && NT % 64 == 0, "channel pairs x token parts");
   constexpr int PARTS = NT / 64, TPP = QF_D / PARTS;  // K scan: token parts, tokens per part
+  constexpr int TB = 8;                               // V rows per load batch of a warp
   const float qmax = static_cast<float>((1u << BITS) - 1u);
   float4* fs = reinterpret_cast<float4*>(sm);
   __half2* plo = reinterpret_cast<__half2*>(sm + QF_D * 16);
@@ -344,91 +347,106 @@ __device__ __forceinline__ void qf_flush_window(const Geom& G, const __half* rk,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* kp = reinterpret_cast<uint32_t*>(rec + 2 * G.wbytes);
   uint32_t* vp = reinterpret_cast<uint32_t*>(rec + 2 * G.wbytes + G.kp_bytes);
-  for (int hf = 0; hf < G.n_r / QF_D; ++hf) {
-    // ---- K: KChannel group = the tile's 128 tokens of one channel
-    const __half* kt = rk + (size_t)hf * QF_D * QF_D;
-    const __half2* kt2 = reinterpret_cast<const __half2*>(kt);
-    {
-      const int cp = tid % 64, part = tid / 64;
-      const int t0 = part * TPP;
-      __half2 lo = kt2[(size_t)t0 * 64 + cp], hi = lo;
+  const int H = G.n_r / QF_D;
+  for (int item = item0; item < 2 * H; item += istep) {
+    if (item < H) {
+      // ---- K tile hf: KChannel group = the tile's 128 tokens of one channel
+      const int hf = item;
+      const __half* kt = rk + (size_t)hf * QF_D * QF_D;
+      const __half2* kt2 = reinterpret_cast<const __half2*>(kt);
+      {
+        const int cp = tid % 64, part = tid / 64;
+        const int t0 = part * TPP;
+        __half2 lo = kt2[(size_t)t0 * 64 + cp], hi = lo;
 #pragma unroll 16
-      for (int t = t0 + 1; t < t0 + TPP; ++t) {
-        const __half2 x = kt2[(size_t)t * 64 + cp];
-        lo = __hmin2(lo, x);
-        hi = __hmax2(hi, x);
+        for (int t = t0 + 1; t < t0 + TPP; ++t) {
+          const __half2 x = kt2[(size_t)t * 64 + cp];
+          lo = __hmin2(lo, x);
+          hi = __hmax2(hi, x);
+        }
+        plo[part * 64 + cp] = lo;
+        phi[part * 64 + cp] = hi;
       }
-      plo[part * 64 + cp] = lo;
-      phi[part * 64 + cp] = hi;
-    }
-    named_bar(bar, NT);
-    for (int ch = tid; ch < QF_D; ch += NT) {
-      float lo = INFINITY, hi = -INFINITY;
+      named_bar(bar, NT);
+      for (int ch = tid; ch < QF_D; ch += NT) {
+        float lo = INFINITY, hi = -INFINITY;
 #pragma unroll
-      for (int p = 0; p < PARTS; ++p) {
-        const __half2 l2 = plo[p * 64 + ch / 2], h2 = phi[p * 64 + ch / 2];
-        lo = fminf(lo, __half2float((ch & 1) ? __high2half(l2) : __low2half(l2)));
-        hi = fmaxf(hi, __half2float((ch & 1) ? __high2half(h2) : __low2half(h2)));
+        for (int p = 0; p < PARTS; ++p) {
+          const __half2 l2 = plo[p * 64 + ch / 2], h2 = phi[p * 64 + ch / 2];
+          lo = fminf(lo, __half2float((ch & 1) ? __high2half(l2) : __low2half(l2)));
+          hi = fmaxf(hi, __half2float((ch & 1) ? __high2half(h2) : __low2half(h2)));
+        }
+        if (lo == 0.f || hi == 0.f) {  // sign of the first zero in token order
+          for (int t = 0; t < QF_D; ++t) {
+            const float x = __half2float(kt[(size_t)t * QF_D + ch]);
+            if (x == 0.f) {
+              if (lo == 0.f) lo = x;
+              if (hi == 0.f) hi = x;
+              break;
+            }
+          }
+        }
+        float s, z;
+        group_params(lo, hi, qmax, s, z);
+        fs[ch] = make_float4(s, z, __frcp_rn(s), 0.f);
+        kp[hf * QF_D + ch] = param_u32(s, z);
       }
-      if (lo == 0.f || hi == 0.f) {  // sign of the first zero in token order
-        for (int t = 0; t < QF_D; ++t) {
-          const float x = __half2float(kt[(size_t)t * QF_D + ch]);
-          if (x == 0.f) {
+      named_bar(bar, NT);
+      if (G.interleave)
+        qf_pack<BITS, false, true, NT>(kt, fs, rec, G, hf);
+      else
+        qf_pack<BITS, false, false, NT>(kt, fs, rec, G, hf);
+    } else {
+      // ---- V tile hf: token groups (the 128 channels of one token); warp per
+      // token, TB rows of a warp in flight per batch
+      const int hf = item - H;
+      const __half* vt = rv + (size_t)hf * QF_D * QF_D;
+      const __half2* vt2 = reinterpret_cast<const __half2*>(vt);
+      for (int tb = warp * TB; tb < QF_D; tb += (NT / 32) * TB) {
+        __half2 a[TB], b[TB];
+#pragma unroll
+        for (int i = 0; i < TB; ++i) {
+          a[i] = vt2[(size_t)(tb + i) * 64 + lane];
+          b[i] = vt2[(size_t)(tb + i) * 64 + 32 + lane];
+        }
+#pragma unroll
+        for (int i = 0; i < TB; ++i) {
+          const int t = tb + i;
+          const __half2 lo2 = __hmin2(a[i], b[i]), hi2 = __hmax2(a[i], b[i]);
+          float lo = fminf(__low2float(lo2), __high2float(lo2));
+          float hi = fmaxf(__low2float(hi2), __high2float(hi2));
+          // first zero in channel order (channels 2*lane, 2*lane+1, 64+2*lane, ...)
+          int zf = 0x7fffffff;
+          if (__low2float(a[i]) == 0.f) zf = 2 * lane;
+          else if (__high2float(a[i]) == 0.f) zf = 2 * lane + 1;
+          else if (__low2float(b[i]) == 0.f) zf = 64 + 2 * lane;
+          else if (__high2float(b[i]) == 0.f) zf = 65 + 2 * lane;
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+            zf = min(zf, __shfl_xor_sync(0xffffffffu, zf, o));
+          }
+          if (lo == 0.f || hi == 0.f) {
+            const float x = __half2float(vt[(size_t)t * QF_D + zf]);
             if (lo == 0.f) lo = x;
             if (hi == 0.f) hi = x;
-            break;
+          }
+          if (lane == 0) {
+            float s, z;
+            group_params(lo, hi, qmax, s, z);
+            fs[t] = make_float4(s, z, __frcp_rn(s), 0.f);
+            vp[hf * QF_D + t] = param_u32(s, z);
           }
         }
       }
-      float s, z;
-      group_params(lo, hi, qmax, s, z);
-      fs[ch] = make_float4(s, z, __frcp_rn(s), 0.f);
-      kp[hf * QF_D + ch] = param_u32(s, z);
+      named_bar(bar, NT);
+      if (G.interleave)
+        qf_pack<BITS, true, true, NT>(vt, fs, rec + G.wbytes, G, hf);
+      else
+        qf_pack<BITS, true, false, NT>(vt, fs, rec + G.wbytes, G, hf);
     }
-    named_bar(bar, NT);
-    if (G.interleave)
-      qf_pack<BITS, false, true, NT>(kt, fs, rec, G, hf);
-    else
-      qf_pack<BITS, false, false, NT>(kt, fs, rec, G, hf);
     named_bar(bar, NT);  // fs is reused
-    // ---- V: token groups (the 128 channels of one token); warp per token
-    const __half* vt = rv + (size_t)hf * QF_D * QF_D;
-    const __half2* vt2 = reinterpret_cast<const __half2*>(vt);
-    for (int t = warp; t < QF_D; t += NT / 32) {
-      const __half2 a = vt2[(size_t)t * 64 + lane], b = vt2[(size_t)t * 64 + 32 + lane];
-      const __half2 lo2 = __hmin2(a, b), hi2 = __hmax2(a, b);
-      float lo = fminf(__low2float(lo2), __high2float(lo2));
-      float hi = fmaxf(__low2float(hi2), __high2float(hi2));
-      // first zero in channel order (channels 2*lane, 2*lane+1, 64+2*lane, ...)
-      int zf = 0x7fffffff;
-      if (__low2float(a) == 0.f) zf = 2 * lane;
-      else if (__high2float(a) == 0.f) zf = 2 * lane + 1;
-      else if (__low2float(b) == 0.f) zf = 64 + 2 * lane;
-      else if (__high2float(b) == 0.f) zf = 65 + 2 * lane;
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        zf = min(zf, __shfl_xor_sync(0xffffffffu, zf, o));
-      }
-      if (lo == 0.f || hi == 0.f) {
-        const float x = __half2float(vt[(size_t)t * QF_D + zf]);
-        if (lo == 0.f) lo = x;
-        if (hi == 0.f) hi = x;
-      }
-      if (lane == 0) {
-        float s, z;
-        group_params(lo, hi, qmax, s, z);
-        fs[t] = make_float4(s, z, __frcp_rn(s), 0.f);
-        vp[hf * QF_D + t] = param_u32(s, z);
-      }
-    }
-    named_bar(bar, NT);
-    if (G.interleave)
-      qf_pack<BITS, true, true, NT>(vt, fs, rec + G.wbytes, G, hf);
-    else
-      qf_pack<BITS, true, false, NT>(vt, fs, rec + G.wbytes, G, hf);
-    named_bar(bar, NT);
   }
 }
 
