@@ -1006,7 +1006,11 @@ __global__ void __launch_bounds__(D) combine_fast_kernel(const __grid_constant__
   const int cell = blockIdx.x, h = blockIdx.y, ch = threadIdx.x;
   const int ng = a.n_group;
   const Sched S = make_sched(c, a, cells, a.rt);
-  if (a.pdl) pdl_wait();  // the attention grid's partials (and, dev schedule, its lengths)
+  // host schedule: everything but the partials comes from the arguments (or
+  // the schedule upload that precedes the attention grid), so it is worked
+  // out before griddepcontrol.wait; the device schedule reads the lengths
+  // after it
+  if (a.pdl && a.dev_sched) pdl_wait();
   // the cell's unit range [cb, ce) and total T: host schedule from the
   // arguments, device schedule by a block reduction over the lengths
   long long cb, ce, T;
@@ -1057,6 +1061,15 @@ __global__ void __launch_bounds__(D) combine_fast_kernel(const __grid_constant__
   const int nk = hi - lo + 1;
   const int stride = slot_stride(ng);
   const float* base = a.slots + (size_t)(lo + cell) * stride;
+  // the step's commit of this cell (lengths from the arguments when uniform)
+  const bool app = a.k_new != nullptr && !a.skip_residual;
+  int rl0 = a.uni_rl, pb0 = a.uni_pb;
+  if (a.pdl && !a.dev_sched) pdl_wait();  // the attention grid's partials
+  if (!a.uni_len) {
+    rl0 = __ldcg(S.rl() + cell);
+    pb0 = __ldcg(S.pb() + cell);
+  }
+  const bool fill = app && rl0 + 1 == G.n_r;
   // online LSE merge over the contributors, CMB_LB loads of each kind in flight
   float M = -INFINITY, L = 0.f, acc = 0.f;
   for (int k0 = 0; k0 < nk; k0 += CMB_LB) {
@@ -1094,11 +1107,8 @@ __global__ void __launch_bounds__(D) combine_fast_kernel(const __grid_constant__
   const size_t row = (size_t)bidx * a.heads_q + (size_t)hk * ng + h;
   a.out[row * D + ch] = L > 0.f ? acc / L : 0.f;
   if (a.out_lse != nullptr && ch == 0) a.out_lse[row] = L > 0.f ? M + __log2f(L) : -INFINITY;
-  // ---- the step's commit of this cell (every contributor has read the window)
-  const bool app = a.k_new != nullptr && !a.skip_residual;
-  const int rl0 = a.uni_len ? a.uni_rl : __ldcg(S.rl() + cell);
-  const int pb0 = a.uni_len ? a.uni_pb : __ldcg(S.pb() + cell);
-  const bool fill = app && rl0 + 1 == G.n_r;
+  if (h != 0 && !fill) return;
+  // ---- the commit (every contributor has read the window)
   if (fill) {
     // build_block + commit_block (kvcache.cpp:208-237) after the step's
     // attention (attention.cpp:235-240); the cell's n_group CTAs split the
