@@ -519,13 +519,13 @@ def run_decode(args, name, mode, world, rank, local, steps, warmup, e2e_steps, s
                      "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4) if achieved else None,
                      "peak_source": peak_src, "kernel": kern_name,
-                     "duration": "timed region / attention launches (one per step, back to back "
-                                 "with programmatic dependent launch)",
+                     "duration": "timed region / steps (each step = attention grid + combine "
+                                 "grid, back to back with programmatic dependent launch)",
                      "kernel_avg_us": round(step_ms * 1e3, 2),
                      "kernel_isolated_us": round(kern_avg_ms * 1e3, 2),
                      "isolated_achieved": round(iso, 1) if iso else None,
-                     "isolated_note": "CUDA events around each launch (no PDL overlap, includes "
-                                      "launch latency)",
+                     "isolated_note": "CUDA events around each step's launches (no PDL "
+                                      "overlap, includes launch latency)",
                      "algorithmic_bytes_per_launch": round(per_launch_bytes),
                      "traffic": load_traffic(name if mode == "fast" else f"{name}_precise")},
         "e2e": ({"value": round(e2e_total / (e2e_ms_max * 1e-3) / 1e9, 2), "unit": "GB/s",
