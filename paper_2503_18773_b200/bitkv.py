@@ -133,11 +133,16 @@ class AttentionConfig:
         return self.heads_q // self.heads_kv
 
     def _c(self) -> _L.AttnConfig:
+        return self._c_ref()[0]
+
+    def _c_ref(self):
+        """(C struct, reusable byref of it), rebuilt when a field changed."""
         key = (self.batch, self.heads_q, self.heads_kv, self.head_dim, self.tile_m, self.tile_n,
                self.num_splits, self.warp_n, self.warp_m)
         cached = self.__dict__.get("_c_cache")
         if cached is None or cached[0] != key:  # the fields are plain and mutable
-            cached = (key, _L.AttnConfig(*key))
+            st = _L.AttnConfig(*key)
+            cached = (key, (st, C.byref(st)))
             self.__dict__["_c_cache"] = cached
         return cached[1]
 
@@ -683,11 +688,10 @@ def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None)
     Host arrays in -> numpy out via the host C-ABI entry (H2D/D2H inside);
     ``out`` may then be a C-contiguous float32 numpy array of q's shape to
     reuse across steps."""
-    c = cfg._c()
+    c, c_ref = cfg._c_ref()
     shape_q = (cfg.batch, cfg.heads_q, cfg.head_dim)
     shape_kv = (cfg.batch, cfg.heads_kv, cfg.head_dim)
-    is_dev = torch is not None and isinstance(q, torch.Tensor) and q.is_cuda
-    if not is_dev:
+    if type(q) is np.ndarray or not (torch is not None and isinstance(q, torch.Tensor) and q.is_cuda):
         qh = np.ascontiguousarray(q, np.float32)
         kh = np.ascontiguousarray(k_new, np.float32)
         vh = np.ascontiguousarray(v_new, np.float32)
@@ -703,7 +707,7 @@ def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None)
         else:
             raise ShapeError(f"decode_step: out must be a writable C-contiguous float32 array "
                              f"of shape {shape_q}")
-        _check(_L.load().bdk_decode_step_host(cache.handle(), C.byref(c), _addr(qh), _addr(kh),
+        _check(_L.load().bdk_decode_step_host(cache.handle(), c_ref, _addr(qh), _addr(kh),
                                               _addr(vh), _addr(o)))
         return AttnOutput(cfg.batch, cfg.heads_q, cfg.head_dim, o)
     if tuple(q.shape) != shape_q or tuple(k_new.shape) != shape_kv or \
