@@ -3,14 +3,16 @@
 # line with extras + parity, per-workload lines, reference arm), flush-step
 # latency, trace stats, ncu launch list + full captures of the hot kernels,
 # and steady-state (application replay, no cache flush) DRAM bytes per launch.
-mkdir -p gpurun_out/r02
-O=gpurun_out/r02
+O=gpurun_out/${OUT:-r02}; mkdir -p $O
+
 python -c "from paper_2503_18773_b200 import build as B; assert not B._stale(), \"stale lib\"" || exit 3
 nvidia-smi -L > $O/gpu.txt 2>&1; lscpu > $O/host_cpu.txt 2>&1
 timeout 1200 python -m pytest tests -m gpu -q -rA > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 1500 python bench.py > $O/bench_default.json 2> $O/bench_default.err
 for w in C5 C2 C3 C1 C2b4; do timeout 600 python bench.py --workload $w --quick --no-cpu-baseline > $O/bench_$w.json 2> $O/bench_$w.err; done
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:combine_fast -s 8 -c 1 -f -o /tmp/prof_cmb python bench.py --workload C5 --quick --steps 5 --warmup 3 --soak 0 --e2e-steps 0 --no-cpu-baseline > $O/ncu_full_combine_C5.log 2>&1
+python tools/ncu_summary.py /tmp/prof_cmb.ncu-rep > $O/ncu_summary_combine_C5.txt 2>&1
 for w in C4 C4b2; do timeout 600 python bench.py --workload $w --quick --steps 100 > $O/bench_$w.json 2> $O/bench_$w.err; done
 timeout 900 python bench.py --impl reference > $O/bench_ref_C5.json 2> $O/bench_ref_C5.err
 python tools/flush_step.py C5 C2 C3 C1 > $O/flush_step.txt 2>&1
