@@ -61,17 +61,33 @@ __device__ __forceinline__ void tma_bulk_s2g(void* dst, const void* src, uint32_
 // product within 1e-4 of a half-integer.  Out of line to keep the fast path
 // small.
 template <int BITS>
-__device__ __noinline__ uint32_t exact_word(const __half* tile, const float4* fs, int tsr, int tw,
-                                            int ch, float4 pk, int interleave) {
+__device__ __noinline__ uint32_t exact_word(const __half* tile, const uint32_t* prm, int tsr, int tw,
+                                            int ch, int interleave) {
   constexpr int P = 16 / BITS;
   const float qmax = static_cast<float>((1u << BITS) - 1u);
   uint32_t word = 0;
   for (int p = 0; p < P; ++p) {
     const int t = tw + pos_token(p, P, interleave);
-    if (tsr != 0) pk = fs[t];
-    word |= quant_code(__half2float(tile[(size_t)t * QF_D + ch]), pk.x, pk.y, qmax) << (p * BITS);
+    const uint32_t u = prm[tsr != 0 ? t : ch];
+    const float s = __half2float(__ushort_as_half(static_cast<uint16_t>(u & 0xFFFFu)));
+    const float z = __half2float(__ushort_as_half(static_cast<uint16_t>(u >> 16)));
+    word |= quant_code(__half2float(tile[(size_t)t * QF_D + ch]), s, z, qmax) << (p * BITS);
   }
   return word;
+}
+
+// Fast-path constants of one group: fs = (tie threshold, z, 1/s, -z/s).
+// q = fma(x, 1/s, -z/s) differs from the reference's rn(rn(x - z) / s) by at
+// most (qmax + 1) 2^-22 + |z/s| 2^-24 (the rounding of 1/s, of -z/s, of the
+// FMA, and the reference's own roundings of x - z and of the quotient), so a
+// q farther than 4x that from a half-integer rounds like the reference; the
+// others take the exact path (exact_word).  Constant groups (s = kMinScale,
+// huge |z/s|) get a negative threshold: always exact.
+__device__ __forceinline__ float4 qf_group_consts(float s, float z, float qmax) {
+  const float r = __frcp_rn(s);
+  const float c = -__fmul_rn(z, r);
+  const float margin = 4.f * ((qmax + 1.f) * (1.f / 4194304.f) + fabsf(c) * (1.f / 16777216.f));
+  return make_float4(0.5f - margin, z, r, c);
 }
 
 // codes + pack of one 128-token tile (tokens [hf*128, hf*128+128) of the
@@ -84,8 +100,8 @@ __device__ __noinline__ uint32_t exact_word(const __half* tile, const float4* fs
 // [0, qmax + 0.5).
 // (NT: threads [0, NT) of the CTA take part; `tile` may be shared or global)
 template <int BITS, bool TOKEN_PARAMS, bool IL, int NT = QF_THREADS>
-__device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, uint8_t* words,
-                                        const Geom& G, int hf) {
+__device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, const uint32_t* prm,
+                                        uint8_t* words, const Geom& G, int hf) {
   constexpr int P = 16 / BITS;
   constexpr int CPT = QF_D / (8 * P);  // 16-byte chunks per row in one tile
   // SPLIT threads share a chunk (4 / SPLIT word pairs each) so that all
@@ -99,9 +115,6 @@ __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, ui
   int tok[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) tok[p] = pos_token(p, P, IL ? 1 : 0);
-  // |q - x/s| <= 2^-22 q: a product farther than 4 * 2^-22 * (qmax + 1) from a
-  // half-integer rounds like the exact quotient
-  constexpr float TIE = 0.5f - 4.f * (1.f / 4194304.f) * (float)(1 << BITS);
   // q + 1.5 * 2^23 lands in [2^23, 2^24), where the ulp is 1: the FADD rounds q
   // to an integer (ties to even, as rintf) and leaves it in the low mantissa
   // bits, so rint + float->int costs one FADD instead of two XU-pipe ops.  The
@@ -136,21 +149,21 @@ __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, ui
           const int t = tw + tok[p];
           if (TOKEN_PARAMS) pa = pb = fs[t];
           const float2 x = __half22float2(tile2[(size_t)t * 64 + cp]);
-          // fmaxf maps a NaN quotient (a non-finite group) to code 0, as the
-          // reference's clamp + cast does on x86; in-group quotients are >= 0
-          const float q0 = fmaxf(__fmul_rn(__fsub_rn(x.x, pa.y), pa.z), 0.f);
-          const float q1 = fmaxf(__fmul_rn(__fsub_rn(x.y, pb.y), pb.z), 0.f);
+          // q = (x - z) / s as one FMA (qf_group_consts); fmaxf maps a NaN
+          // quotient to code 0, as the reference's clamp + cast does on x86
+          const float q0 = fmaxf(__fmaf_rn(x.x, pa.z, pa.w), 0.f);
+          const float q1 = fmaxf(__fmaf_rn(x.y, pb.z, pb.w), 0.f);
           const float t0m = __fadd_rn(q0, MAGIC), t1m = __fadd_rn(q1, MAGIC);
           const float r0 = __fsub_rn(t0m, MAGIC), r1 = __fsub_rn(t1m, MAGIC);
-          tie |= (fabsf(q0 - r0) > TIE) | (fabsf(q1 - r1) > TIE);
+          tie |= (fabsf(q0 - r0) > pa.x) | (fabsf(q1 - r1) > pb.x);
           a0 += __float_as_uint(t0m) << (p * BITS);
           a1 += __float_as_uint(t1m) << (p * BITS);
         }
         a0 -= bias;
         a1 -= bias;
         if (__any_sync(0xffffffffu, tie) && tie) {
-          a0 = exact_word<BITS>(tile, fs, TOKEN_PARAMS, tw, 2 * cp, pa, G.interleave);
-          a1 = exact_word<BITS>(tile, fs, TOKEN_PARAMS, tw, 2 * cp + 1, pb, G.interleave);
+          a0 = exact_word<BITS>(tile, prm, TOKEN_PARAMS, tw, 2 * cp, G.interleave);
+          a1 = exact_word<BITS>(tile, prm, TOKEN_PARAMS, tw, 2 * cp + 1, G.interleave);
         }
         p0 |= a0 << (16 * h);
         p1 |= a1 << (16 * h);
@@ -268,7 +281,7 @@ __global__ void __launch_bounds__(QF_THREADS) qpack_fast_kernel(DevCache c, cons
       }
       float s, z;
       group_params(lo, hi, qmax, s, z);
-      fs[ch] = make_float4(s, z, __frcp_rn(s), 0.f);
+      fs[ch] = qf_group_consts(s, z, qmax);
       pout[ch] = param_u32(s, z);
     }
   } else {
@@ -299,7 +312,7 @@ __global__ void __launch_bounds__(QF_THREADS) qpack_fast_kernel(DevCache c, cons
       }
       float s, z;
       group_params(flo, fhi, qmax, s, z);
-      fs[t] = make_float4(s, z, __frcp_rn(s), 0.f);
+      fs[t] = qf_group_consts(s, z, qmax);
       pout[t] = param_u32(s, z);
     }
   }
@@ -312,14 +325,14 @@ __global__ void __launch_bounds__(QF_THREADS) qpack_fast_kernel(DevCache c, cons
   }
   if (tsr == 0) {
     if (G.interleave)
-      qf_pack<BITS, false, true>(tile, fs, rec, G, hf);
+      qf_pack<BITS, false, true>(tile, fs, pout, rec, G, hf);
     else
-      qf_pack<BITS, false, false>(tile, fs, rec, G, hf);
+      qf_pack<BITS, false, false>(tile, fs, pout, rec, G, hf);
   } else {
     if (G.interleave)
-      qf_pack<BITS, true, true>(tile, fs, rec + G.wbytes, G, hf);
+      qf_pack<BITS, true, true>(tile, fs, pout, rec + G.wbytes, G, hf);
     else
-      qf_pack<BITS, true, false>(tile, fs, rec + G.wbytes, G, hf);
+      qf_pack<BITS, true, false>(tile, fs, pout, rec + G.wbytes, G, hf);
   }
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
@@ -388,14 +401,14 @@ __device__ __forceinline__ void qf_flush_window(const Geom& G, const __half* rk,
         }
         float s, z;
         group_params(lo, hi, qmax, s, z);
-        fs[ch] = make_float4(s, z, __frcp_rn(s), 0.f);
+        fs[ch] = qf_group_consts(s, z, qmax);
         kp[hf * QF_D + ch] = param_u32(s, z);
       }
       named_bar(bar, NT);
       if (G.interleave)
-        qf_pack<BITS, false, true, NT>(kt, fs, rec, G, hf);
+        qf_pack<BITS, false, true, NT>(kt, fs, kp + hf * QF_D, rec, G, hf);
       else
-        qf_pack<BITS, false, false, NT>(kt, fs, rec, G, hf);
+        qf_pack<BITS, false, false, NT>(kt, fs, kp + hf * QF_D, rec, G, hf);
     } else {
       // ---- V tile hf: token groups (the 128 channels of one token); warp per
       // token, TB rows of a warp in flight per batch
@@ -435,16 +448,16 @@ __device__ __forceinline__ void qf_flush_window(const Geom& G, const __half* rk,
           if (lane == 0) {
             float s, z;
             group_params(lo, hi, qmax, s, z);
-            fs[t] = make_float4(s, z, __frcp_rn(s), 0.f);
+            fs[t] = qf_group_consts(s, z, qmax);
             vp[hf * QF_D + t] = param_u32(s, z);
           }
         }
       }
       named_bar(bar, NT);
       if (G.interleave)
-        qf_pack<BITS, true, true, NT>(vt, fs, rec + G.wbytes, G, hf);
+        qf_pack<BITS, true, true, NT>(vt, fs, vp + hf * QF_D, rec + G.wbytes, G, hf);
       else
-        qf_pack<BITS, true, false, NT>(vt, fs, rec + G.wbytes, G, hf);
+        qf_pack<BITS, true, false, NT>(vt, fs, vp + hf * QF_D, rec + G.wbytes, G, hf);
     }
     named_bar(bar, NT);  // fs is reused
   }

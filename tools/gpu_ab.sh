@@ -15,7 +15,7 @@ import json, sys
 try:
     d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
     e = d.get("e2e") or {}
-    print(f"{sys.argv[3]:4s} {sys.argv[2]:10s} value={d['value']:8.1f} frac={d['roofline']['frac']:.3f} us={d.get('latency_us', d.get('ms_per_step',0)*1e3):7.2f} iso_us={d['roofline']['kernel_isolated_us']:7.2f} e2e={e.get('value')} e2e_us={e.get('latency_us')}")
+    print(f"{sys.argv[3]:4s} {sys.argv[2]:10s} value={d['value']:8.1f} frac={d['roofline']['frac']:.3f} us={d.get('latency_us', d.get('ms_per_step',0)*1e3):7.2f} iso_us={d['roofline'].get('kernel_isolated_us') or 0:7.2f} e2e={e.get('value')} e2e_us={e.get('latency_us')}")
 except Exception as ex:
     print(sys.argv[3], sys.argv[2], "FAILED", ex)
 PY
