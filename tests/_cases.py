@@ -57,8 +57,12 @@ def adversarial_data(c: Case, seed: int):
     k[..., 5] = -0.0                      # a channel of -0
     k[..., 7] = 7.25                      # a constant channel
     k[..., 9] = rng.normal(0, 300, shape[:-1]).astype(np.float16).astype(np.float32)
+    # a large offset with a small spread (|z/s| ~ 1e4): the fast quantizer's
+    # FMA form needs its widest tie margin here
+    k[..., 11] = 1000.0 + 0.5 * rng.integers(0, 4, shape[:-1])
     v[:, :, ::17, :] = -0.0               # all-zero tokens
     v[:, :, 1::19, :] = 3.0               # constant tokens
+    v[:, :, 2::23, :] = 500.0 + 0.25 * rng.integers(0, 5, v[:, :, 2::23, :].shape)
     return k.astype(np.float16).astype(np.float32), v.astype(np.float16).astype(np.float32)
 
 

@@ -105,6 +105,39 @@ def test_prefill_adversarial_bit_exact(bits, warp_n):
     assert_same_cache(c, gpu_cache(c, k, v), oracle_cache(c, k, v))
 
 
+@pytest.mark.parametrize("bits", [4, 2])
+def test_fused_flush_of_adversarial_windows_bit_exact(bits):
+    """The fast step's fused flush (the combine grid's qf_flush_window, split
+    over the cell's n_group CTAs) on adversarial windows: exact .5 quotients,
+    +-0 extrema, constant and large-offset channels/tokens, filled by decode
+    appends; every block bit-exact against the oracle after the flush."""
+    bk = _bk()
+    n_r = 8 * 4 * (16 // bits)
+    c = Case(bits=bits, warp_n=4, heads_q=8, heads_kv=2, batch=2, prefill=2 * n_r + n_r - 3,
+             steps=5, seed=40 + bits)
+    k, v = adversarial_data(c, c.seed)
+    # the appended rows come from a second adversarial sample
+    c2 = Case(bits=bits, warp_n=4, heads_q=8, heads_kv=2, batch=2, prefill=c.steps, seed=c.seed + 1)
+    ka, va = adversarial_data(c2, c2.seed)
+    oc = oracle_cache(c, k, v)
+    gc = gpu_cache(c, k, v)
+    gc.set_precise(False)
+    cfg = bk.AttentionConfig(batch=c.batch, heads_q=c.heads_q, heads_kv=c.heads_kv, head_dim=D,
+                             warp_n=4)
+    from oracle import oracle as O
+    g = O.Gauss(c.seed)
+    for s in range(c.steps):
+        q = g.rounded(c.batch * c.heads_q * D).reshape(c.batch, c.heads_q, D)
+        kn = np.ascontiguousarray(ka[:, :, s, :])
+        vn = np.ascontiguousarray(va[:, :, s, :])
+        oc.decode_step(q, kn, vn)
+        got = bk.decode_step(gc, cfg, torch.from_numpy(q).cuda().half(),
+                             torch.from_numpy(kn).cuda().half(),
+                             torch.from_numpy(vn).cuda().half()).data.cpu().numpy()
+        assert np.isfinite(got).all()
+    assert_same_cache(c, gc, oc)
+
+
 def test_reset_then_prefill_again():
     from oracle import oracle as O
     c = Case(bits=2, warp_n=4, heads_kv=2, batch=2, prefill=3 * 256 + 11, seed=21)
