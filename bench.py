@@ -252,9 +252,20 @@ def load_traffic(key):
         return None
 
 
+def oversubscribed(world):
+    """Dev knob BDK_BENCH_OVERSUB=1: more ranks than GPUs share them (rank r
+    on GPU r % count, gloo process group) -- exercises the N-rank plumbing,
+    the head/sequence split and the peer-memory exchange on one GPU; its
+    timings mean nothing."""
+    import torch
+    return os.environ.get("BDK_BENCH_OVERSUB") == "1" and world > torch.cuda.device_count()
+
+
 def peer_ok(world, local):
     """True when this GPU can map every peer's memory (P2P over NVLink)."""
     import torch
+    if oversubscribed(world):  # every rank's buffers on this GPU: CUDA IPC, no peer link
+        return True
     return all(torch.cuda.can_device_access_peer(local, p) for p in range(world) if p != local)
 
 
@@ -1004,7 +1015,11 @@ def main():
         return
     import torch
     import torch.distributed as dist
-    if world > 1:
+    if world > 1 and oversubscribed(world):
+        local = local % torch.cuda.device_count()
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+    elif world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:

@@ -49,3 +49,24 @@ def test_reference_arm_honours_warmup_and_config():
     assert j["impl"] == "reference" and j["warmup"] == 4 and j["steps"] == 3
     assert j["config"] == bench.workload_config("C1", 1)
     assert j["cpu_baseline"]["kind"] == "reference" and j["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload,kind", [("C5", "seq-split2"), ("C3", "kv-head-shard2"), ("C2", "dp2")])
+def test_two_rank_bench_on_one_gpu(workload, kind):
+    """--gpus 2 end to end with both ranks on one GPU (BDK_BENCH_OVERSUB: gloo
+    process group, rank r on GPU r % count): the sequence split with the
+    peer-memory merge, the KV-head shard and the replicas run and report
+    a whole-job line.  Timings of an oversubscribed GPU mean nothing."""
+    env_prev = os.environ.get("BDK_BENCH_OVERSUB")
+    os.environ["BDK_BENCH_OVERSUB"] = "1"
+    try:
+        j = _run("--gpus", "2", "--workload", workload, "--quick", "--no-cpu-baseline",
+                 "--steps", "5", "--warmup", "3", "--e2e-steps", "2", "--soak", "0", timeout=600)
+    finally:
+        if env_prev is None:
+            os.environ.pop("BDK_BENCH_OVERSUB", None)
+        else:
+            os.environ["BDK_BENCH_OVERSUB"] = env_prev
+    assert j["n_gpus"] == 2 and j["value"] > 0 and j["gpu_launches"] > 0
+    assert j["config"]["parallelism"].startswith(kind), j["config"]
