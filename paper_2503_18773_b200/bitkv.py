@@ -132,19 +132,27 @@ class AttentionConfig:
     def n_group(self) -> int:
         return self.heads_q // self.heads_kv
 
+    def __setattr__(self, name, value):
+        # the fields are plain and mutable: a change drops the cached C struct
+        self.__dict__.pop("_c_cache", None)
+        object.__setattr__(self, name, value)
+
     def _c(self) -> _L.AttnConfig:
         return self._c_ref()[0]
 
     def _c_ref(self):
-        """(C struct, reusable byref of it), rebuilt when a field changed."""
-        key = (self.batch, self.heads_q, self.heads_kv, self.head_dim, self.tile_m, self.tile_n,
-               self.num_splits, self.warp_n, self.warp_m)
+        """(C struct, reusable byref of it, its address, q / k_new element
+        counts, q / kv shapes), built on first use after a field change."""
         cached = self.__dict__.get("_c_cache")
-        if cached is None or cached[0] != key:  # the fields are plain and mutable
+        if cached is None:
+            key = (self.batch, self.heads_q, self.heads_kv, self.head_dim, self.tile_m,
+                   self.tile_n, self.num_splits, self.warp_n, self.warp_m)
             st = _L.AttnConfig(*key)
-            cached = (key, (st, C.byref(st)))
+            sq = (self.batch, self.heads_q, self.head_dim)
+            skv = (self.batch, self.heads_kv, self.head_dim)
+            cached = (st, C.byref(st), C.addressof(st), math.prod(sq), math.prod(skv), sq, skv)
             self.__dict__["_c_cache"] = cached
-        return cached[1]
+        return cached
 
 
 def validate_config(cfg: AttentionConfig) -> AttentionConfig:
@@ -672,6 +680,31 @@ def load_cache_file(path: str, *, max_tokens: int = 0, device: int = 0) -> KVCac
     return KVCache._adopt(h, header, device)
 
 
+_PYHOST = None
+
+
+def _pyhost():
+    """(step, address of bdk_decode_step_host) of the CPython fast path
+    (csrc/bdk_pyhost.c, built in-tree next to the library), or False."""
+    global _PYHOST
+    if _PYHOST is None:
+        _PYHOST = False
+        try:
+            import importlib.util
+            import os
+            from . import build as _B
+            path = _B.pyhost_path()
+            if os.path.exists(path):
+                spec = importlib.util.spec_from_file_location("_bdk_pyhost", path)
+                mod = importlib.util.module_from_spec(spec)
+                spec.loader.exec_module(mod)
+                fn = C.cast(_L.load().bdk_decode_step_host, C.c_void_p).value
+                _PYHOST = (mod.step, fn)
+        except Exception:
+            _PYHOST = False
+    return _PYHOST
+
+
 def _addr(a: np.ndarray) -> int:
     """Data address of a C-contiguous array (the cheap way for writable
     buffers; ``ndarray.ctypes`` builds an object per access)."""
@@ -688,9 +721,19 @@ def decode_step(cache: KVCache, cfg: AttentionConfig, q, k_new, v_new, out=None)
     Host arrays in -> numpy out via the host C-ABI entry (H2D/D2H inside);
     ``out`` may then be a C-contiguous float32 numpy array of q's shape to
     reuse across steps."""
-    c, c_ref = cfg._c_ref()
-    shape_q = (cfg.batch, cfg.heads_q, cfg.head_dim)
-    shape_kv = (cfg.batch, cfg.heads_kv, cfg.head_dim)
+    c, c_ref, c_addr, nq, nkv, shape_q, shape_kv = cfg._c_ref()
+    if type(q) is np.ndarray and type(k_new) is np.ndarray and type(v_new) is np.ndarray \
+            and type(out) is np.ndarray and q.shape == shape_q and k_new.shape == shape_kv \
+            and v_new.shape == shape_kv and out.shape == shape_q:
+        # the steady host loop: float32 C-contiguous arrays straight into the
+        # C-ABI through the buffer protocol (csrc/bdk_pyhost.c); anything else
+        # (other dtypes / layouts) takes the general path below
+        ph = _pyhost()
+        if ph:
+            st = ph[0](ph[1], cache._h.value, c_addr, q, k_new, v_new, out, nq, nkv)
+            if st != -1000:
+                _check(st)
+                return AttnOutput(cfg.batch, cfg.heads_q, cfg.head_dim, out)
     if type(q) is np.ndarray or not (torch is not None and isinstance(q, torch.Tensor) and q.is_cuda):
         qh = np.ascontiguousarray(q, np.float32)
         kh = np.ascontiguousarray(k_new, np.float32)

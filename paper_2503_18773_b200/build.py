@@ -34,6 +34,7 @@ def _stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
+        build_pyhost()
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     objs = []
@@ -52,7 +53,31 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc failed")
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fopenmp", "-o", LIB, *objs]
     subprocess.run(cmd, check=True)
+    build_pyhost(force=True)
     return LIB
+
+
+PYHOST_SRC = os.path.join(CSRC, "bdk_pyhost.c")
+
+
+def pyhost_path() -> str:
+    import sysconfig
+    return os.path.join(LIBDIR, "_bdk_pyhost" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+
+
+def build_pyhost(force: bool = False) -> str | None:
+    """The CPython fast path of the host decode call (csrc/bdk_pyhost.c);
+    None when no C compiler / Python headers (bitkv then keeps to ctypes)."""
+    import sysconfig
+    out = pyhost_path()
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(PYHOST_SRC):
+        return out
+    inc = sysconfig.get_paths().get("include")
+    if not inc or not os.path.exists(os.path.join(inc, "Python.h")):
+        return None
+    os.makedirs(LIBDIR, exist_ok=True)
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-I", inc, PYHOST_SRC, "-o", out]
+    return out if subprocess.run(cmd).returncode == 0 else None
 
 
 if __name__ == "__main__":
