@@ -46,7 +46,8 @@ struct DecodeArgs {
 };
 
 // Fast decode (bdk_decode_fast.cu): stream-K over (cell, unit) with unit =
-// one packed block or the residual window of a cell; in-kernel LSE combine.
+// one packed block or the residual window of a cell; the LSE combine, the
+// length commit and the fused flush run in the combine grid launched after it.
 struct FastArgs {
   const __half* q = nullptr;      // [batch][heads_q][d]
   const __half* k_new = nullptr;  // [batch][heads_kv][d] (nullptr: no append)
