@@ -1065,6 +1065,7 @@ __global__ void __launch_bounds__(D) combine_fast_kernel(const __grid_constant__
   const bool app = a.k_new != nullptr && !a.skip_residual;
   int rl0 = a.uni_rl, pb0 = a.uni_pb;
   if (a.pdl && !a.dev_sched) pdl_wait();  // the attention grid's partials
+  if (a.dev_flags & 8) return;  // dev probe: the combine grid's cost in the step
   if (!a.uni_len) {
     rl0 = __ldcg(S.rl() + cell);
     pb0 = __ldcg(S.pb() + cell);
