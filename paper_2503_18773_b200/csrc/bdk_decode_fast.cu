@@ -139,6 +139,12 @@ __device__ __forceinline__ Sched make_sched(const DevCache& c, const FastArgs& a
   return Sched{&c, &a, cells, rt};
 }
 
+__device__ __forceinline__ int ld_acquire_gpu_i(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 struct SchedOut {
   long long T, off0;  // total units; first unit of cell0
   int cell0;
@@ -860,6 +866,11 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   }
   // q, lengths, counters and slots: after the previous kernel
   if (a.pdl && !a.dev_sched) pdl_wait();
+  // the previous step's completion counters (its combine grid has finished)
+  // start the next step at zero
+  if (a.done != nullptr && warp < NC)
+    for (int i = blockIdx.x * (NC * 32) + threadIdx.x; i < cells; i += gridDim.x * (NC * 32))
+      a.done[(size_t)(a.par ^ 1) * cells + i] = 0;
 
   // ---------------------------------------------------------- prep warps
   if (warp > NC) {
@@ -966,6 +977,11 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     if (tr && threadIdx.x == 0) tr[3] = globaltimer();
     float* slot = a.slots + (size_t)(blockIdx.x + cell) * stride_slot;
     finalize_segment<NC, CP>(st, o, merge_sm, ng, slot, oscale_seg);  // ends with a barrier
+    // the segment's partial is complete: count it for the combine grid (the
+    // barrier orders every consumer thread's slot writes before this release)
+    if (a.done != nullptr && threadIdx.x == 0)
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.done + (size_t)a.par * cells + cell)
+                   : "memory");
     if (tr && threadIdx.x == 0) tr[4] = globaltimer();
     if (tr && threadIdx.x == 0) {
       tr[5] = globaltimer();
@@ -1064,7 +1080,17 @@ __global__ void __launch_bounds__(D) combine_fast_kernel(const __grid_constant__
   // the step's commit of this cell (lengths from the arguments when uniform)
   const bool app = a.k_new != nullptr && !a.skip_residual;
   int rl0 = a.uni_rl, pb0 = a.uni_pb;
-  if (a.pdl && !a.dev_sched) pdl_wait();  // the attention grid's partials
+  if (a.done != nullptr && !a.dev_sched) {
+    // host schedule: start as soon as this cell's nk partials are written
+    // (the attention grid's CTAs count them), not when its last CTA exits
+    if (threadIdx.x == 0) {
+      const int* cnt = a.done + (size_t)a.par * cells + cell;
+      while (ld_acquire_gpu_i(cnt) < nk) __nanosleep(64);
+    }
+    __syncthreads();
+  } else if (a.pdl && !a.dev_sched) {
+    pdl_wait();  // the attention grid's partials
+  }
   if (a.dev_flags & 8) return;  // dev probe: the combine grid's cost in the step
   if (!a.uni_len) {
     rl0 = __ldcg(S.rl() + cell);
