@@ -53,6 +53,7 @@ struct bdk_cache {
   int graphs = 0;                     // live bdk_graph objects (workspaces are pinned)
   float* slots = nullptr;             // device partial slots
   int* done = nullptr;                // device [2][cells] partials written per cell
+  bool done_live = false;             // the last fast step kept `done` counted
   size_t slot_floats = 0;
   int fast_ctas_per_sm = -1, fast_ng = -1;
   // attention-kernel timing (bdk_profile_begin/end): one event pair per launch
@@ -284,15 +285,19 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
     BDK_CUDA(cudaMalloc(&c->slots, need * sizeof(float)), "cudaMalloc(slots)");
     c->slot_floats = need;
   }
-  if (!c->done) {
-    BDK_CUDA(cudaMalloc(&c->done, 2 * cells * sizeof(int)), "cudaMalloc(done)");
-    BDK_CUDA(cudaMemsetAsync(c->done, 0, 2 * cells * sizeof(int), stream), "memset(done)");
-  }
+  if (!c->done) BDK_CUDA(cudaMalloc(&c->done, 2 * cells * sizeof(int)), "cudaMalloc(done)");
   bdk::FastArgs a;
   // the combine grid starts on per-cell completion counts when it is small
   // enough to sit resident beside the attention grid's tail (C1, C2, C5);
   // a large one (C3: 1024 CTAs) waits for the grid instead (measured)
-  a.done = (size_t)cells * ng <= (size_t)n_ctas ? c->done : nullptr;
+  a.spin = (size_t)cells * ng <= (size_t)n_ctas ? 1 : 0;
+  // counted only when the combine spins on them (the release adds cost a
+  // fence per segment: C3's 1024 cells); a step that starts counting again
+  // after steps that did not finds both parities zeroed
+  if (a.spin && !c->done_live)
+    BDK_CUDA(cudaMemsetAsync(c->done, 0, 2 * cells * sizeof(int), stream), "memset(done)");
+  c->done_live = a.spin != 0;
+  a.done = a.spin ? c->done : nullptr;
   a.q = static_cast<const __half*>(q);
   a.k_new = static_cast<const __half*>(k_new);
   a.v_new = static_cast<const __half*>(v_new);

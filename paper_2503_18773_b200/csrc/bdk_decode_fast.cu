@@ -1080,7 +1080,7 @@ __global__ void __launch_bounds__(D) combine_fast_kernel(const __grid_constant__
   // the step's commit of this cell (lengths from the arguments when uniform)
   const bool app = a.k_new != nullptr && !a.skip_residual;
   int rl0 = a.uni_rl, pb0 = a.uni_pb;
-  if (a.done != nullptr && !a.dev_sched) {
+  if (a.spin && a.done != nullptr && !a.dev_sched) {
     // host schedule: start as soon as this cell's nk partials are written
     // (the attention grid's CTAs count them), not when its last CTA exits
     if (threadIdx.x == 0) {

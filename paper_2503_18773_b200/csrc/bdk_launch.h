@@ -55,8 +55,8 @@ struct FastArgs {
   float* out = nullptr;      // [batch][heads_q][d]
   float* out_lse = nullptr;  // optional [batch][heads_q] (log2 domain)
   float* slots = nullptr;    // [n_ctas + cells][n_group][d + 2] partials
-  int* done = nullptr;       // [2][cells] partials written per cell (by step parity; host
-                             // schedule: the combine grid starts on them)
+  int* done = nullptr;       // [2][cells] partials written per cell, by step parity
+  int spin = 0;              // host schedule: the combine grid starts on `done` counts
   int n_ctas = 0, heads_q = 0, n_group = 0;
   int blk_begin = 0, blk_end = 1 << 30;  // packed block range attended
   int skip_residual = 0;  // residual units attend nothing (sequence-split ranks)
