@@ -477,3 +477,34 @@ def test_peer_merge_sequence_split_on_streams(world):
             err = (outs[r] - full_o.view(rows, D)).abs().max().item()
             assert err < 1e-5, (r, err)
             assert (lses[r] - full_lse.view(rows)).abs().max().item() < 1e-4
+
+
+def test_combine_start_mode_changes_between_steps():
+    """The combine grid starts on per-cell completion counts only when it is
+    small (cells x n_group <= the attention grid); alternating the query group
+    size on one cache switches the counting off and on between steps, and the
+    counters must restart from zero every time (bdk_api.cu: done_live)."""
+    bk = _bk()
+    from oracle import oracle as O
+    batch, hkv, prefill = 36, 8, 300  # 288 cells: n_group 1 counts, n_group 2 does not
+    c = Case(bits=4, warp_n=4, heads_q=hkv, heads_kv=hkv, batch=batch, prefill=prefill,
+             steps=6, seed=77)
+    g = O.Gauss(c.seed)
+    k, v = prefill_data(c, g)
+    oc = oracle_cache(c, k, v)
+    gc = gpu_cache(c, k, v)
+    gc.set_precise(False)
+    worst = {"max_abs": 0.0, "rel_l2": 0.0}
+    for s in range(c.steps):
+        hq = hkv * (1 + s % 2)
+        cfg = bk.AttentionConfig(batch=batch, heads_q=hq, heads_kv=hkv, head_dim=D, warp_n=4)
+        q = g.rounded(batch * hq * D).reshape(batch, hq, D)
+        kn = g.rounded(batch * hkv * D).reshape(batch, hkv, D)
+        vn = g.rounded(batch * hkv * D).reshape(batch, hkv, D)
+        ref = oc.decode_step(q, kn, vn)
+        got = bk.decode_step(gc, cfg, torch.from_numpy(q).cuda().half(),
+                             torch.from_numpy(kn).cuda().half(),
+                             torch.from_numpy(vn).cuda().half()).data.cpu().numpy()
+        e = errors(got, ref)
+        worst = {kk: max(worst[kk], e[kk]) for kk in worst}
+    check_tol(worst, False)
