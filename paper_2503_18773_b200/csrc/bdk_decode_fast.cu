@@ -499,20 +499,27 @@ __device__ __forceinline__ void prep_loop(const DevCache& c, const FastArgs& a, 
 }
 
 // One packed block (one 16-byte chunk j of every channel row) of a consumer
-// warp: S^T = codes_K . Q'^T, online softmax, O^T += codes_V^T . P'^T.
+// warp, in four stages (so the consumer loop can software-pipeline them):
+//   qk_stage   S^T = codes_K . Q'^T -> logits (log2 domain, zero term folded)
+//   soft_stage online softmax, zero term, P' = P * s_t -> P'^T fragments
+//   ldv_stage  ldmatrix of the V words into registers, release of the stage
+//   pv_stage   O^T += codes_V^T . P'^T
 // `rec` is the staged block record, `qp` its folded query (prep warp).
 template <int BITS, int WN, int CP>
-__device__ __forceinline__ void consume_block(const uint8_t* rec, const uint8_t* qp, const Geom& G,
-                                              int j, float scale,
-                                              const int (&vtok)[FC<BITS, WN, 1, 1>::NPAIR / CP][2],
-                                              Soft& st, float (&o)[OT][4], uint64_t* empty_s,
-                                              int dev_flags) {
+struct Stg {
   using C = FC<BITS, WN, 1, 1>;
-  constexpr int P = C::P, NPAIR = C::NPAIR, RB = C::RB;
-  constexpr int NPK = NPAIR / CP;
-  constexpr int SH_REF = BITS == 8 ? 0 : 2;
-  const int lane = threadIdx.x & 31, gid = lane >> 2, t4 = lane & 3;
-      const uint32_t* vpr = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes + G.kp_bytes);
+  static constexpr int P = C::P, NPAIR = C::NPAIR, RB = C::RB;
+  static constexpr int NPK = NPAIR / CP;
+  static constexpr int NPH = CP == 2 ? NPK : 1;
+  static constexpr int SH_REF = BITS == 8 ? 0 : 2;
+};
+
+template <int BITS, int WN, int CP>
+__device__ __forceinline__ void qk_stage(const uint8_t* rec, const uint8_t* qp, int j, float scale,
+                                         float (&sacc)[Stg<BITS, WN, CP>::NPK][4]) {
+  using T = Stg<BITS, WN, CP>;
+  constexpr int P = T::P, NPAIR = T::NPAIR, RB = T::RB, NPK = T::NPK;
+  const int lane = threadIdx.x & 31, t4 = lane & 3;
   // Q'^T B fragments (ldmatrix of the [head][channel] rows; rows >= n_group
   // are zero).  CP = 2: qh = the same heads in columns 4..7 (each lane's
   // row address is r ^ 4, so columns 0..3 read the zero rows 4..7)
@@ -581,7 +588,6 @@ __device__ __forceinline__ void consume_block(const uint8_t* rec, const uint8_t*
       }
     }
   }
-  float sacc[NPK][4];
 #pragma unroll
   for (int i = 0; i < NPK; ++i)
 #pragma unroll
@@ -591,9 +597,9 @@ __device__ __forceinline__ void consume_block(const uint8_t* rec, const uint8_t*
       for (int k = 1; k < NCH / NPK; ++k) x += chn[i + k * NPK][r];
       sacc[i][r] = x;
     }
-  // ---- logits (log2 domain), online softmax
-  // S = S' 2^(24 - sh) + Z (rows gid / gid+8 hold fields 2i / 2i+1; the
-  // partner tile i + HALF has the same field shifts), in the log2 domain
+  // ---- logits (log2 domain): S = S' 2^(24 - sh) + Z (rows gid / gid+8
+  // hold fields 2i / 2i+1; the partner tile i + HALF has the same field
+  // shifts)
 #pragma unroll
   for (int i = 0; i < NPK; ++i) {
     const float al = scale * (float)(1 << (24 - ((2 * i) % P) * BITS % 8));
@@ -603,9 +609,21 @@ __device__ __forceinline__ void consume_block(const uint8_t* rec, const uint8_t*
     sacc[i][2] = fmaf(sacc[i][2], ah, zs0);
     sacc[i][3] = fmaf(sacc[i][3], ah, zs1);
   }
+}
+
+template <int BITS, int WN, int CP>
+__device__ __forceinline__ void soft_stage(const uint8_t* rec, const Geom& G, int j,
+                                           const int (&vtok)[Stg<BITS, WN, CP>::NPK][2],
+                                           float (&sacc)[Stg<BITS, WN, CP>::NPK][4], Soft& st,
+                                           float (&o)[OT][4],
+                                           uint32_t (&pb)[Stg<BITS, WN, CP>::NPK][2],
+                                           uint32_t (&pbh)[Stg<BITS, WN, CP>::NPH][2]) {
+  using T = Stg<BITS, WN, CP>;
+  constexpr int P = T::P, NPK = T::NPK, SH_REF = T::SH_REF;
+  const int lane = threadIdx.x & 31, gid = lane >> 2;
+  const uint32_t* vpr = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes + G.kp_bytes);
   softmax_update<NPK>(sacc, st, o);
   // ---- P' = P * s_t (V token scale folded), zero term, P'^T fragments
-  uint32_t pb[NPK][2];
 #pragma unroll
   for (int i = 0; i < NPK; ++i) {
     // V (scale, zero) of the tokens of rows gid / gid+8 (fields 2i / 2i+1
@@ -626,7 +644,6 @@ __device__ __forceinline__ void consume_block(const uint8_t* rec, const uint8_t*
   }
   // CP = 2: P'^T of tile i keeps only its column half (head columns n =
   // gid after the transpose)
-  uint32_t pbh[CP == 2 ? NPK : 1][2];
   if constexpr (CP == 2) {
 #pragma unroll
     for (int i = 0; i < NPK; ++i) {
@@ -636,25 +653,40 @@ __device__ __forceinline__ void consume_block(const uint8_t* rec, const uint8_t*
       pb[i][1] = gid < 4 ? pb[i][1] : 0u;
     }
   }
-  // ---- O^T += codes_V^T . P'^T
-  {
-    const uint32_t vw = smem_u32(rec + G.wbytes);
-    uint32_t vr[4][4];
+}
+
+// V words of the chunk into registers; then the ring slot and its prep slot
+// are free (every read of the stage is done)
+template <int BITS, int WN, int CP>
+__device__ __forceinline__ void ldv_stage(const uint8_t* rec, const Geom& G, int j,
+                                          uint32_t (&vr)[4][4], uint64_t* empty_s) {
+  constexpr int RB = Stg<BITS, WN, CP>::RB;
+  const int lane = threadIdx.x & 31;
+  const uint32_t vw = smem_u32(rec + G.wbytes);
 #pragma unroll
-    for (int vc = 0; vc < 4; ++vc) {
-      const int row = vc * 32 + lane;
-      ldsm_x4(vw + row * RB + ((j ^ swz(row, WN)) << 4), vr[vc][0], vr[vc][1], vr[vc][2],
-              vr[vc][3]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty_s);  // ring slot + prep slot are free
+  for (int vc = 0; vc < 4; ++vc) {
+    const int row = vc * 32 + lane;
+    ldsm_x4(vw + row * RB + ((j ^ swz(row, WN)) << 4), vr[vc][0], vr[vc][1], vr[vc][2], vr[vc][3]);
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty_s);  // ring slot + prep slot are free
+}
+
+template <int BITS, int WN, int CP>
+__device__ __forceinline__ void pv_stage(const uint32_t (&vr)[4][4],
+                                         const uint32_t (&pb)[Stg<BITS, WN, CP>::NPK][2],
+                                         const uint32_t (&pbh)[Stg<BITS, WN, CP>::NPH][2],
+                                         float (&o)[OT][4]) {
+  using T = Stg<BITS, WN, CP>;
+  constexpr int P = T::P, NPAIR = T::NPAIR, NPK = T::NPK;
+  constexpr int HALF = NPAIR / 2;
 #pragma unroll
-    for (int mt = 0; mt < KT; ++mt) {
-      const uint32_t ra = vr[mt / 2][2 * (mt % 2)], rb = vr[mt / 2][2 * (mt % 2) + 1];
-      const uint32_t ra8 = ra >> 8, rb8 = rb >> 8;
+  for (int mt = 0; mt < KT; ++mt) {
+    const uint32_t ra = vr[mt / 2][2 * (mt % 2)], rb = vr[mt / 2][2 * (mt % 2) + 1];
+    const uint32_t ra8 = ra >> 8, rb8 = rb >> 8;
 #pragma unroll
-      for (int pi = 0; pi < NPAIR; ++pi) {
-        uint32_t af[4];
+    for (int pi = 0; pi < NPAIR; ++pi) {
+      uint32_t af[4];
 #define BDK_VEXT(PI)                                 \
   if (pi == PI) {                                    \
     af[0] = ext_sub<BITS, (2 * PI) % P>(ra, ra8);     \
@@ -662,18 +694,32 @@ __device__ __forceinline__ void consume_block(const uint8_t* rec, const uint8_t*
     af[2] = ext_sub<BITS, (2 * PI + 1) % P>(ra, ra8); \
     af[3] = ext_sub<BITS, (2 * PI + 1) % P>(rb, rb8); \
   }
-        BDK_VEXT(0)
-        BDK_VEXT(1)
-        BDK_VEXT(2)
-        BDK_VEXT(3)
+      BDK_VEXT(0)
+      BDK_VEXT(1)
+      BDK_VEXT(2)
+      BDK_VEXT(3)
 #undef BDK_VEXT
-        if (CP == 2 && pi >= HALF)
-          mma16816(o[mt], af, pbh[CP == 2 ? pi - HALF : 0][0], pbh[CP == 2 ? pi - HALF : 0][1]);
-        else
-          mma16816(o[mt], af, pb[pi % NPK][0], pb[pi % NPK][1]);
-      }
+      if (CP == 2 && pi >= HALF)
+        mma16816(o[mt], af, pbh[CP == 2 ? pi - HALF : 0][0], pbh[CP == 2 ? pi - HALF : 0][1]);
+      else
+        mma16816(o[mt], af, pb[pi % NPK][0], pb[pi % NPK][1]);
     }
   }
+}
+
+// The four stages back to back (the unpipelined consumer).
+template <int BITS, int WN, int CP>
+__device__ __forceinline__ void consume_block(const uint8_t* rec, const uint8_t* qp, const Geom& G,
+                                              int j, float scale,
+                                              const int (&vtok)[Stg<BITS, WN, CP>::NPK][2],
+                                              Soft& st, float (&o)[OT][4], uint64_t* empty_s) {
+  using T = Stg<BITS, WN, CP>;
+  float sacc[T::NPK][4];
+  uint32_t pb[T::NPK][2], pbh[T::NPH][2], vr[4][4];
+  qk_stage<BITS, WN, CP>(rec, qp, j, scale, sacc);
+  soft_stage<BITS, WN, CP>(rec, G, j, vtok, sacc, st, o, pb, pbh);
+  ldv_stage<BITS, WN, CP>(rec, G, j, vr, empty_s);
+  pv_stage<BITS, WN, CP>(vr, pb, pbh, o);
 }
 
 // Residual tokens [t_lo, t_hi) of `cell` (fp16 window, residual_attend,
@@ -757,7 +803,7 @@ __device__ __forceinline__ void consume_residual(const DevCache& c, const FastAr
   }
 }
 
-template <int BITS, int WN, int NS, int MINB, int GRP, int CP>
+template <int BITS, int WN, int NS, int MINB, int GRP, int CP, int SWP>
 __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     decode_fast_kernel(const __grid_constant__ DevCache c, const __grid_constant__ FastArgs a) {
   using C = FC<BITS, WN, MINB, GRP>;
@@ -923,7 +969,54 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     // dynamically from a shared-memory counter, so the groups stay busy to
     // the end of the cell whatever the warp scheduler favours
     const int it_end = it + (int)max(0LL, pk_end - u);
-    int kn = GRP > 1 ? claim_next(claim + j, lane) : it;
+    if constexpr (SWP) {
+      // software-pipelined consumer (GRP == 1): block k's QK^T is issued in
+      // the same basic block as block k-1's PV (independent HMMA chains and
+      // extraction for the scheduler to interleave); block k-1's V words are
+      // already in registers and its stage released.  The O updates keep the
+      // unpipelined order (PV(k-1) before softmax(k)'s rescale): bit-identical.
+      static_assert(GRP == 1, "the pipelined consumer walks its blocks in order");
+      using TS = Stg<BITS, WN, CP>;
+      if (a.dev_flags & 1) {  // dev probe: stream only (no compute)
+        for (int k = it; k < it_end; ++k) {
+          const int s = k % NS;
+          mbar_wait(&ready[s], (k / NS) & 1);
+          mbar_wait(&full[s], (k / NS) & 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        }
+      } else if (it < it_end) {
+        float sacc[TS::NPK][4];
+        uint32_t pb[TS::NPK][2], pbh[TS::NPH][2], vr[4][4];
+        {
+          const int s = it % NS;
+          mbar_wait(&ready[s], (it / NS) & 1);
+          mbar_wait(&full[s], (it / NS) & 1);
+          if (tr && threadIdx.x == 0 && it == 0) tr[1] = globaltimer();
+          const uint8_t* rec = ring + (size_t)s * REC;
+          qk_stage<BITS, WN, CP>(rec, prep + (size_t)s * L.prep_stride + kgr * QP_BYTES, j, scale,
+                                 sacc);
+          soft_stage<BITS, WN, CP>(rec, G, j, vtok, sacc, st, o, pb, pbh);
+          ldv_stage<BITS, WN, CP>(rec, G, j, vr, &empty[s]);
+        }
+        for (int k = it + 1; k < it_end; ++k) {
+          const int s = k % NS;
+          unsigned long long tw = 0;
+          if (tr && threadIdx.x == 0) tw = globaltimer();
+          mbar_wait(&ready[s], (k / NS) & 1);
+          mbar_wait(&full[s], (k / NS) & 1);
+          if (tr && threadIdx.x == 0) tr[9] += globaltimer() - tw;
+          const uint8_t* rec = ring + (size_t)s * REC;
+          qk_stage<BITS, WN, CP>(rec, prep + (size_t)s * L.prep_stride + kgr * QP_BYTES, j, scale,
+                                 sacc);
+          pv_stage<BITS, WN, CP>(vr, pb, pbh, o);
+          soft_stage<BITS, WN, CP>(rec, G, j, vtok, sacc, st, o, pb, pbh);
+          ldv_stage<BITS, WN, CP>(rec, G, j, vr, &empty[s]);
+        }
+        pv_stage<BITS, WN, CP>(vr, pb, pbh, o);
+      }
+    }
+    int kn = SWP ? it_end : (GRP > 1 ? claim_next(claim + j, lane) : it);
     for (int k = kn; k < it_end; k = kn) {
       kn = GRP > 1 ? claim_next(claim + j, lane) : k + 1;  // next claim, in flight
       const int s = k % NS;
@@ -942,7 +1035,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
       }
       consume_block<BITS, WN, CP>(ring + (size_t)s * REC,
                                   prep + (size_t)s * L.prep_stride + kgr * QP_BYTES, G, j, scale,
-                                  vtok, st, o, &empty[s], a.dev_flags);
+                                  vtok, st, o, &empty[s]);
     }
 
     it = it_end;
@@ -1178,15 +1271,34 @@ struct Variant {
   const void* combine;  // combine_fast_kernel of the same geometry
 };
 
+// software-pipelined consumer loop (GRP == 1 kernels); dev knob BDK_SWP=0|1
+static int swp_knob() {
+  static int v = [] {
+    const char* e = getenv("BDK_SWP");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <int BITS, int WN, int NS, int MINB, int GRP>
-static Variant variant(int cp) {
+static Variant variant(int cp, bool swp) {
   const void* comb = reinterpret_cast<const void*>(combine_fast_kernel<BITS, WN>);
   if constexpr (BITS != 8) {
-    if (cp == 2)
-      return Variant{reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP, 2>),
+    if (cp == 2) {
+      if constexpr (GRP == 1)
+        if (swp)
+          return Variant{
+              reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP, 2, 1>), NS,
+              GRP, comb};
+      return Variant{reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP, 2, 0>),
                      NS, GRP, comb};
+    }
   }
-  return Variant{reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP, 1>), NS,
+  if constexpr (GRP == 1)
+    if (swp)
+      return Variant{reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP, 1, 1>),
+                     NS, GRP, comb};
+  return Variant{reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP, 1, 0>), NS,
                  GRP, comb};
 }
 
@@ -1202,15 +1314,18 @@ static int variant_knob() {
 // (measured best on B200).  Dev knob BDK_FAST_VARIANT: 2 = one CTA per SM with
 // two consumer groups claiming chunks from a shared 8-stage ring, 3 = three
 // groups at 128 registers (both measured 6-15% slower).
-static Variant fast_kernel(const Geom& G, int ng) {
+// swp: the software-pipelined consumer loop (measured: C5 +3.8%, C2 +-0.3%;
+// C1, under one block per CTA, -3%: chosen when CTAs average >= 2 blocks)
+static Variant fast_kernel(const Geom& G, int ng, bool swp = true) {
   const int v = variant_knob();
+  swp = swp && swp_knob() != 0;
   // dev knob BDK_COLPACK: 0 = never, 2 = wherever the layout allows (4-bit too)
   static const int cp_knob = getenv("BDK_COLPACK") ? atoi(getenv("BDK_COLPACK")) : -1;
   const int cp = cp_knob == 0 ? 1
                  : cp_knob == 2 ? ((ng <= 4 && (G.bits == 2 || G.bits == 4)) ? 2 : 1)
                                 : col_pack(G, ng);
 #define BDK_SEL(B, W, NS, MB, GR) \
-  if (G.bits == B && G.warp_n == W) return variant<B, W, NS, MB, GR>(cp);
+  if (G.bits == B && G.warp_n == W) return variant<B, W, NS, MB, GR>(cp, swp);
   if (v == 2) {
     BDK_SEL(2, 4, 8, 1, 2) BDK_SEL(4, 4, 8, 1, 2)
   } else if (v == 3) {
@@ -1248,7 +1363,9 @@ int fast_decode_ctas_per_sm(const Geom& G, int n_group) {
 }
 
 cudaError_t launch_decode_fast(const DevCache& c, const FastArgs& a, cudaStream_t s) {
-  const Variant k = fast_kernel(c.G, a.n_group);
+  // graph steps (device schedule) hold for any lengths: pipelined
+  const bool swp = a.dev_sched || a.total_units >= 2LL * a.n_ctas;
+  const Variant k = fast_kernel(c.G, a.n_group, swp);
   if (!k.fn) return cudaErrorInvalidValue;
   const uint32_t smem = fast_smem(c.G, a.n_group, k);
   DevCache cc = c;
