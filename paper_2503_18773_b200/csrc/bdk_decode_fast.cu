@@ -377,13 +377,21 @@ __device__ __forceinline__ void finalize_segment(Soft st, float (&o)[OT][4], flo
   named_bar(1, NC * 32);
 }
 
+// f32 += f16 * f16 as one FHFMA (sm_100): the product of two binary16 values
+// is exact in fp32, so this equals fmaf(float(a), float(b), c) bit for bit
+__device__ __forceinline__ float fhfma(uint16_t a, uint16_t b, float c) {
+  asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(c) : "h"(a), "h"(b));
+  return c;
+}
+
 // Fold of one staged block for the prep warp: Q'[h][c] = fp16(q[h][c] s_c)
-// and Z[h] = sum_c q[h][c] z_c for every K group of the block (q2 / qf: this
-// lane's query channels as half2 / fp32).
+// and Z[h] = sum_c q[h][c] z_c for every K group of the block (q2: this
+// lane's query channels as half2).  The params are (scale | zero << 16) u32
+// per channel; the zero terms take the high halves directly (FHFMA half
+// selects: no conversions, no repacking).
 template <int NH>
 __device__ __forceinline__ void prep_fold(const uint8_t* rec, uint8_t* pp, const Geom& G, int ng,
-                                          const uint32_t (&q2)[D / (32 / NH) / 2],
-                                          const float (&qf)[D / (32 / NH)]) {
+                                          const uint32_t (&q2)[D / (32 / NH) / 2]) {
   constexpr int LPH = 32 / NH;  // lanes per head
   constexpr int CPL = D / LPH;  // channels per lane
   constexpr int H2 = CPL / 2;   // half2 per lane
@@ -395,15 +403,31 @@ __device__ __forceinline__ void prep_fold(const uint8_t* rec, uint8_t* pp, const
     uint8_t* qp = pp + gr * QP_BYTES;
     float za = 0.f, zb = 0.f;
     uint32_t qo[H2];
+    uint32_t pw[CPL];
+    if constexpr (CPL % 4 == 0) {
+#pragma unroll
+      for (int v = 0; v < CPL / 4; ++v) {
+        const uint4 x = *reinterpret_cast<const uint4*>(kp + gr * D + cbk * CPL + 4 * v);
+        pw[4 * v] = x.x;
+        pw[4 * v + 1] = x.y;
+        pw[4 * v + 2] = x.z;
+        pw[4 * v + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < CPL / 2; ++v) {
+        const uint2 x = *reinterpret_cast<const uint2*>(kp + gr * D + cbk * CPL + 2 * v);
+        pw[2 * v] = x.x;
+        pw[2 * v + 1] = x.y;
+      }
+    }
 #pragma unroll
     for (int i = 0; i < H2; ++i) {
-      const uint2 pr = *reinterpret_cast<const uint2*>(kp + gr * D + cbk * CPL + 2 * i);
-      const __half2 s2 = u2h(prmt(pr.x, pr.y, 0x5410));
-      const __half2 z2 = u2h(prmt(pr.x, pr.y, 0x7632));
+      const uint32_t p0 = pw[2 * i], p1 = pw[2 * i + 1];
+      const __half2 s2 = u2h(prmt(p0, p1, 0x5410));
       qo[i] = h2u(__hmul2(u2h(q2[i]), s2));
-      const float2 zf = __half22float2(z2);
-      za = fmaf(qf[2 * i], zf.x, za);
-      zb = fmaf(qf[2 * i + 1], zf.y, zb);
+      za = fhfma((uint16_t)(q2[i] & 0xFFFFu), (uint16_t)(p0 >> 16), za);
+      zb = fhfma((uint16_t)(q2[i] >> 16), (uint16_t)(p1 >> 16), zb);
     }
     if (h < ng) {
       uint32_t* dst = reinterpret_cast<uint32_t*>(qp + h * QP_ROW + cbk * CPL * 2);
@@ -462,7 +486,6 @@ __device__ __forceinline__ void prep_loop(const DevCache& c, const FastArgs& a, 
     if (u < pk_end) {
       const int bidx = cell / G.heads_kv, hk = cell % G.heads_kv;
       uint32_t q2[H2];
-      float qf[CPL];
 #pragma unroll
       for (int i = 0; i < H2; ++i) q2[i] = 0u;
       if (h < ng) {
@@ -470,12 +493,6 @@ __device__ __forceinline__ void prep_loop(const DevCache& c, const FastArgs& a, 
             a.q + ((size_t)bidx * a.heads_q + (size_t)hk * ng + h) * D + cbk * CPL);
 #pragma unroll
         for (int i = 0; i < H2; ++i) q2[i] = __ldg(qs + i);
-      }
-#pragma unroll
-      for (int i = 0; i < H2; ++i) {
-        const float2 f = __half22float2(u2h(q2[i]));
-        qf[2 * i] = f.x;
-        qf[2 * i + 1] = f.y;
       }
       for (long long x = u; x < pk_end; ++x, ++it) {
         if (GRP > 1 && (it % GRP) != px.pgrp) continue;
@@ -485,8 +502,7 @@ __device__ __forceinline__ void prep_loop(const DevCache& c, const FastArgs& a, 
         const unsigned long long tb = (px.tr && lane == 0) ? globaltimer() : 0ull;
         if (px.tr && lane == 0) px.tr[12] += tb - tw;
         if (!(a.dev_flags & 2)) {
-          prep_fold<NH>(px.ring + (size_t)s * px.rec, px.prep + (size_t)s * px.prep_stride, G, ng, q2,
-                        qf);
+          prep_fold<NH>(px.ring + (size_t)s * px.rec, px.prep + (size_t)s * px.prep_stride, G, ng, q2);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&px.ready[s]);
@@ -1352,9 +1368,11 @@ int fast_decode_ctas_per_sm(const Geom& G, int n_group) {
   const Variant k = fast_kernel(G, n_group);
   if (!k.fn) return 0;
   const uint32_t smem = fast_smem(G, n_group, k);
-  if (cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return 0;
+  // both consumer-loop variants (launch_decode_fast picks one per step)
+  for (const bool swp : {true, false})
+    if (cudaFuncSetAttribute(fast_kernel(G, n_group, swp).fn,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k.fn, fast_threads(G, k), smem) !=
       cudaSuccess)

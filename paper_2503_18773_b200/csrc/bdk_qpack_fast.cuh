@@ -149,13 +149,15 @@ __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, co
           const int t = tw + tok[p];
           if (TOKEN_PARAMS) pa = pb = fs[t];
           const float2 x = __half22float2(tile2[(size_t)t * 64 + cp]);
-          // q = (x - z) / s as one FMA (qf_group_consts); fmaxf maps a NaN
-          // quotient to code 0, as the reference's clamp + cast does on x86
-          const float q0 = fmaxf(__fmaf_rn(x.x, pa.z, pa.w), 0.f);
-          const float q1 = fmaxf(__fmaf_rn(x.y, pb.z, pb.w), 0.f);
+          // q = (x - z) / s as one FMA (qf_group_consts).  The tie test is
+          // written unordered (!(d <= thr)): a NaN or infinite quotient fails
+          // it and takes the exact path, which gives the reference's code
+          // (clamp + cast on x86) -- no fmaxf per code
+          const float q0 = __fmaf_rn(x.x, pa.z, pa.w);
+          const float q1 = __fmaf_rn(x.y, pb.z, pb.w);
           const float t0m = __fadd_rn(q0, MAGIC), t1m = __fadd_rn(q1, MAGIC);
           const float r0 = __fsub_rn(t0m, MAGIC), r1 = __fsub_rn(t1m, MAGIC);
-          tie |= (fabsf(q0 - r0) > pa.x) | (fabsf(q1 - r1) > pb.x);
+          tie |= !(fabsf(q0 - r0) <= pa.x) | !(fabsf(q1 - r1) <= pb.x);
           a0 += __float_as_uint(t0m) << (p * BITS);
           a1 += __float_as_uint(t1m) << (p * BITS);
         }
