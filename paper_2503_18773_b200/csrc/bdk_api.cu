@@ -312,6 +312,18 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
   a.skip_residual = no_res ? 1 : 0;
   a.sm_scale_log2 = (1.0f / std::sqrt(static_cast<float>(cfg->head_dim))) * bdk::kLog2e;
   a.par = static_cast<int>(c->fast_steps & 1);
+  // schedule weight of a cell's residual tail + segment switch: 3 extra
+  // (empty) units when CTAs average >= 2 packed blocks (measured: C5 +2.2%,
+  // C2 +4.3%, C3 +0.5%; C1, under one block per CTA, loses with it).  Any
+  // value gives the same partials' union, so graph steps keep the one they
+  // were captured with.  Dev knob BDK_RESW overrides.
+  {
+    static const int resw_knob = getenv("BDK_RESW") ? atoi(getenv("BDK_RESW")) : -1;
+    long long nb_all = 0;
+    for (int i = 0; i < cells; ++i)
+      nb_all += std::max(0, std::min(blk_end, c->packed_blocks[i]) - blk_begin);
+    a.res_extra = resw_knob >= 0 ? resw_knob : (nb_all >= 2LL * n_ctas ? 3 : 0);
+  }
   static const bool dev_sched_knob = getenv("BDK_DEVSCHED") && atoi(getenv("BDK_DEVSCHED")) == 1;
   if (dev_sched_knob) dev_sched = true;
   a.dev_sched = dev_sched ? 1 : 0;
@@ -323,7 +335,7 @@ bdk_status run_decode_fast(bdk_cache* c, const bdk_attn_config* cfg, const void*
     for (int i = 0; i < cells; ++i) {
       const int nb = std::max(0, std::min(blk_end, c->packed_blocks[i]) - blk_begin);
       const int rlen = no_res ? 0 : c->res_len[i] + (k_new != nullptr ? 1 : 0);
-      off[i + 1] = off[i] + nb + std::max(1, (rlen + rt - 1) / rt);
+      off[i + 1] = off[i] + nb + std::max(1, (rlen + rt - 1) / rt) + a.res_extra;
       off[cells + 1 + i] = nb;
     }
     bool uni = true;

@@ -131,7 +131,7 @@ struct Sched {
   __device__ __forceinline__ int units(int cell, int nbc) const {
     if (!a->dev_sched)
       return a->uni_units ? a->uni_units : __ldg(a->unit_off + cell + 1) - __ldg(a->unit_off + cell);
-    return nbc + max(1, (rlen(cell) + rt - 1) / rt);
+    return nbc + max(1, (rlen(cell) + rt - 1) / rt) + a->res_extra;
   }
 };
 

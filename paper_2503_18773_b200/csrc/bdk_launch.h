@@ -71,6 +71,10 @@ struct FastArgs {
   long long total_units = 0;
   int uni_units = 0, uni_nb = 0;
   int uni_len = 0, uni_pb = 0, uni_rl = 0;  // host schedule: every cell has these lengths
+  // extra (empty) residual units per cell: the schedule charges a cell's
+  // residual tail + segment switch this many more blocks' worth of time, so
+  // the CTAs that hold one take fewer packed blocks
+  int res_extra = 0;
   const int* unit_off = nullptr;
   const int* unit_nb = nullptr;
   float sm_scale_log2 = 0.f;

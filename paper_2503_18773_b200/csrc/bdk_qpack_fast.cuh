@@ -99,9 +99,20 @@ __device__ __forceinline__ float4 qf_group_consts(float s, float z, float qmax) 
 // s >= (hi - lo) / qmax * (1 - 2^-11), so every in-group quotient lies in
 // [0, qmax + 0.5).
 // (NT: threads [0, NT) of the CTA take part; `tile` may be shared or global)
+// max(|a|, |b|, c) with NaN propagation (one FMNMX3.NAN): a NaN or infinite
+// quotient's deviation reaches the tie test below
+__device__ __forceinline__ float absmax3_nan(float a, float b, float c) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(fabsf(a)), "f"(fabsf(b)), "f"(c));
+  return d;
+}
+
+// wthr (TOKEN_PARAMS): per word of P tokens, the smallest tie threshold of its
+// tokens (V: one (scale, zero) per token), so a word needs one compare
 template <int BITS, bool TOKEN_PARAMS, bool IL, int NT = QF_THREADS>
 __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, const uint32_t* prm,
-                                        uint8_t* words, const Geom& G, int hf) {
+                                        uint8_t* words, const Geom& G, int hf,
+                                        const float* wthr = nullptr) {
   constexpr int P = 16 / BITS;
   constexpr int CPT = QF_D / (8 * P);  // 16-byte chunks per row in one tile
   // SPLIT threads share a chunk (4 / SPLIT word pairs each) so that all
@@ -131,9 +142,12 @@ __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, co
     const int t0 = jl * 8 * P + sp * NP * 2 * P;  // first token (tile-relative)
     const int j = hf * CPT + jl;                   // chunk index in the row
     float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa;
+    float thr = 0.f;
     if (!TOKEN_PARAMS) {
       pa = fs[2 * cp];
       pb = fs[2 * cp + 1];
+      // the pair's words go to the exact path together: one threshold
+      thr = fminf(pa.x, pb.x);
     }
     uint32_t w0[NP], w1[NP];
 #pragma unroll
@@ -143,26 +157,29 @@ __device__ __forceinline__ void qf_pack(const __half* tile, const float4* fs, co
       for (int h = 0; h < 2; ++h) {
         const int tw = t0 + (i2 * 2 + h) * P;  // first token of the word
         uint32_t a0 = 0, a1 = 0;
-        bool tie = false;
+        // largest |q - rint(q)| over the word's codes of both channels (NaN
+        // propagating); the word pair takes the exact path when it reaches
+        // the threshold
+        float dev = 0.f;
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           const int t = tw + tok[p];
           if (TOKEN_PARAMS) pa = pb = fs[t];
           const float2 x = __half22float2(tile2[(size_t)t * 64 + cp]);
-          // q = (x - z) / s as one FMA (qf_group_consts).  The tie test is
-          // written unordered (!(d <= thr)): a NaN or infinite quotient fails
-          // it and takes the exact path, which gives the reference's code
-          // (clamp + cast on x86) -- no fmaxf per code
+          // q = (x - z) / s as one FMA (qf_group_consts)
           const float q0 = __fmaf_rn(x.x, pa.z, pa.w);
           const float q1 = __fmaf_rn(x.y, pb.z, pb.w);
           const float t0m = __fadd_rn(q0, MAGIC), t1m = __fadd_rn(q1, MAGIC);
           const float r0 = __fsub_rn(t0m, MAGIC), r1 = __fsub_rn(t1m, MAGIC);
-          tie |= !(fabsf(q0 - r0) <= pa.x) | !(fabsf(q1 - r1) <= pb.x);
+          dev = absmax3_nan(q0 - r0, q1 - r1, dev);
           a0 += __float_as_uint(t0m) << (p * BITS);
           a1 += __float_as_uint(t1m) << (p * BITS);
         }
         a0 -= bias;
         a1 -= bias;
+        // unordered: a NaN or infinite quotient (NaN deviation) takes the
+        // exact path, which gives the reference's code (clamp + cast on x86)
+        const bool tie = !(dev <= (TOKEN_PARAMS ? wthr[tw / P] : thr));
         if (__any_sync(0xffffffffu, tie) && tie) {
           a0 = exact_word<BITS>(tile, prm, TOKEN_PARAMS, tw, 2 * cp, G.interleave);
           a1 = exact_word<BITS>(tile, prm, TOKEN_PARAMS, tw, 2 * cp + 1, G.interleave);
@@ -228,6 +245,7 @@ __global__ void __launch_bounds__(QF_THREADS) qpack_fast_kernel(DevCache c, cons
   const __half2* tile2 = reinterpret_cast<const __half2*>(tile);
   uint32_t* pout = reinterpret_cast<uint32_t*>(smem + L.pout);
   float4* fs = reinterpret_cast<float4*>(smem + L.fs);
+  float* wthr_sm = reinterpret_cast<float*>(smem + L.part);  // V: per-word tie threshold
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
   constexpr uint32_t TILE_BYTES = QF_D * QF_D * 2;
   const __half* src = (tsr ? v : k) + (size_t)blockIdx.y * len * QF_D +
@@ -314,8 +332,15 @@ __global__ void __launch_bounds__(QF_THREADS) qpack_fast_kernel(DevCache c, cons
       }
       float s, z;
       group_params(flo, fhi, qmax, s, z);
-      fs[t] = qf_group_consts(s, z, qmax);
+      const float4 k4 = qf_group_consts(s, z, qmax);
+      fs[t] = k4;
       pout[t] = param_u32(s, z);
+      // the word of tokens [t & ~(P-1), +P): smallest tie threshold
+      constexpr int P = 16 / BITS;
+      float wt = k4.x;
+#pragma unroll
+      for (int o = 1; o < P; o <<= 1) wt = fminf(wt, __shfl_xor_sync(0xffffffffu, wt, o));
+      if (t % P == 0) wthr_sm[t / P] = wt;
     }
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -332,9 +357,9 @@ __global__ void __launch_bounds__(QF_THREADS) qpack_fast_kernel(DevCache c, cons
       qf_pack<BITS, false, false>(tile, fs, pout, rec, G, hf);
   } else {
     if (G.interleave)
-      qf_pack<BITS, true, true>(tile, fs, pout, rec + G.wbytes, G, hf);
+      qf_pack<BITS, true, true>(tile, fs, pout, rec + G.wbytes, G, hf, wthr_sm);
     else
-      qf_pack<BITS, true, false>(tile, fs, pout, rec + G.wbytes, G, hf);
+      qf_pack<BITS, true, false>(tile, fs, pout, rec + G.wbytes, G, hf, wthr_sm);
   }
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
@@ -456,10 +481,20 @@ __device__ __forceinline__ void qf_flush_window(const Geom& G, const __half* rk,
         }
       }
       named_bar(bar, NT);
+      // per word of P tokens: the smallest tie threshold (qf_pack)
+      constexpr int P = 16 / BITS;
+      float* wthr = reinterpret_cast<float*>(plo);
+      for (int w = tid; w < QF_D / P; w += NT) {
+        float wt = fs[w * P].x;
+#pragma unroll
+        for (int i = 1; i < P; ++i) wt = fminf(wt, fs[w * P + i].x);
+        wthr[w] = wt;
+      }
+      named_bar(bar, NT);
       if (G.interleave)
-        qf_pack<BITS, true, true, NT>(vt, fs, vp + hf * QF_D, rec + G.wbytes, G, hf);
+        qf_pack<BITS, true, true, NT>(vt, fs, vp + hf * QF_D, rec + G.wbytes, G, hf, wthr);
       else
-        qf_pack<BITS, true, false, NT>(vt, fs, vp + hf * QF_D, rec + G.wbytes, G, hf);
+        qf_pack<BITS, true, false, NT>(vt, fs, vp + hf * QF_D, rec + G.wbytes, G, hf, wthr);
     }
     named_bar(bar, NT);  // fs is reused
   }
