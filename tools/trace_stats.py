@@ -22,8 +22,9 @@ print("finalize         ", q((a[:, 4] - a[:, 3]) / 1e3))
 print("atomic+merge     ", q((a[:, 5] - a[:, 4]) / 1e3))
 print("end (abs)        ", q((a[:, 5] - t0) / 1e3))
 m = a[:, 6] > 0
-print("merge (last CTAs)", q((a[m, 5] - a[m, 4]) / 1e3), "n=", m.sum())
-if a.shape[1] > 10 and (a[m, 10] > 0).all():
+if m.any():  # round-1 in-kernel merge stamps (the combine grid has none)
+    print("merge (last CTAs)", q((a[m, 5] - a[m, 4]) / 1e3), "n=", m.sum())
+if m.any() and a.shape[1] > 10 and (a[m, 10] > 0).all():
     print("  of which atomic ", q((a[m, 10] - a[m, 4]) / 1e3))
     print("  merge_cell      ", q((a[m, 5] - a[m, 10]) / 1e3))
     m2 = m & (a[:, 14] > 0) & (a[:, 15] > 0)  # merge_cell stamps (merge_cell_few has none)
