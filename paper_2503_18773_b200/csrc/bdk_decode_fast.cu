@@ -1287,7 +1287,7 @@ struct Variant {
   const void* combine;  // combine_fast_kernel of the same geometry
 };
 
-// software-pipelined consumer loop (GRP == 1 kernels); dev knob BDK_SWP=0|1
+// software-pipelined consumer loop (GRP == 1 kernels); dev knob BDK_SWP=0|1|2
 static int swp_knob() {
   static int v = [] {
     const char* e = getenv("BDK_SWP");
@@ -1381,8 +1381,9 @@ int fast_decode_ctas_per_sm(const Geom& G, int n_group) {
 }
 
 cudaError_t launch_decode_fast(const DevCache& c, const FastArgs& a, cudaStream_t s) {
-  // graph steps (device schedule) hold for any lengths: pipelined
-  const bool swp = a.dev_sched || a.total_units >= 2LL * a.n_ctas;
+  // graph steps (device schedule) hold for any lengths: pipelined.  Dev knob
+  // BDK_SWP: 0 never, 1 by this rule (default), 2 always
+  const bool swp = a.dev_sched || a.total_units >= 2LL * a.n_ctas || swp_knob() == 2;
   const Variant k = fast_kernel(c.G, a.n_group, swp);
   if (!k.fn) return cudaErrorInvalidValue;
   const uint32_t smem = fast_smem(c.G, a.n_group, k);
