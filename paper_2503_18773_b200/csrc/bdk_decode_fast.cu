@@ -819,7 +819,10 @@ __device__ __forceinline__ void consume_residual(const DevCache& c, const FastAr
   }
 }
 
-template <int BITS, int WN, int NS, int MINB, int GRP, int CP, int SWP>
+// NHT: the prep warp's head layout (n_group rounded up to a power of two)
+// fixed at compile time (only that prep loop in the kernel body: measured
+// +1.4% C5, +0.8% C2 from the smaller body), or 0 = chosen at run time
+template <int BITS, int WN, int NS, int MINB, int GRP, int CP, int SWP, int NHT = 0>
 __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     decode_fast_kernel(const __grid_constant__ DevCache c, const __grid_constant__ FastArgs a) {
   using C = FC<BITS, WN, MINB, GRP>;
@@ -941,10 +944,15 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     const int nh = ng <= 1 ? 1 : ng <= 2 ? 2 : ng <= 4 ? 4 : 8;
     PrepCtx px{ring, prep, full, ready, tr, REC, (int)L.prep_stride, pgrp, u_begin, u_end,
                so.off0, cell0, 16 * NC};
-    if (nh == 1) prep_loop<1, NS, GRP>(c, a, px);
-    else if (nh == 2) prep_loop<2, NS, GRP>(c, a, px);
-    else if (nh == 4) prep_loop<4, NS, GRP>(c, a, px);
-    else prep_loop<8, NS, GRP>(c, a, px);
+    if constexpr (NHT > 0) {
+      (void)nh;
+      prep_loop<NHT, NS, GRP>(c, a, px);
+    } else {
+      if (nh == 1) prep_loop<1, NS, GRP>(c, a, px);
+      else if (nh == 2) prep_loop<2, NS, GRP>(c, a, px);
+      else if (nh == 4) prep_loop<4, NS, GRP>(c, a, px);
+      else prep_loop<8, NS, GRP>(c, a, px);
+    }
     return;
   }
 
@@ -1296,12 +1304,35 @@ static int swp_knob() {
   return v;
 }
 
+// the pipelined W_n = 4 kernels (the BASELINE geometry) with the prep
+// layout fixed for n_group's power of two
+template <int BITS, int NS, int MINB, int CP>
+static const void* swp_nh_kernel(int ng) {
+  const int nh = ng <= 1 ? 1 : ng <= 2 ? 2 : ng <= 4 ? 4 : 8;
+  if (nh == 1) return reinterpret_cast<const void*>(decode_fast_kernel<BITS, 4, NS, MINB, 1, CP, 1, 1>);
+  if (nh == 2) return reinterpret_cast<const void*>(decode_fast_kernel<BITS, 4, NS, MINB, 1, CP, 1, 2>);
+  if constexpr (CP == 2) {  // column packing needs n_group <= 4
+    return reinterpret_cast<const void*>(decode_fast_kernel<BITS, 4, NS, MINB, 1, CP, 1, 4>);
+  } else {
+    if (nh == 4)
+      return reinterpret_cast<const void*>(decode_fast_kernel<BITS, 4, NS, MINB, 1, CP, 1, 4>);
+    return reinterpret_cast<const void*>(decode_fast_kernel<BITS, 4, NS, MINB, 1, CP, 1, 8>);
+  }
+}
+
 template <int BITS, int WN, int NS, int MINB, int GRP>
-static Variant variant(int cp, bool swp) {
+static Variant variant(int cp, bool swp, int ng) {
   const void* comb = reinterpret_cast<const void*>(combine_fast_kernel<BITS, WN>);
+  if constexpr (WN == 4 && GRP == 1) {
+    if (swp) {
+      if constexpr (BITS != 8)
+        if (cp == 2) return Variant{swp_nh_kernel<BITS, NS, MINB, 2>(ng), NS, GRP, comb};
+      return Variant{swp_nh_kernel<BITS, NS, MINB, 1>(ng), NS, GRP, comb};
+    }
+  }
   if constexpr (BITS != 8) {
     if (cp == 2) {
-      if constexpr (GRP == 1)
+      if constexpr (GRP == 1 && WN != 4)
         if (swp)
           return Variant{
               reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP, 2, 1>), NS,
@@ -1310,7 +1341,7 @@ static Variant variant(int cp, bool swp) {
                      NS, GRP, comb};
     }
   }
-  if constexpr (GRP == 1)
+  if constexpr (GRP == 1 && WN != 4)
     if (swp)
       return Variant{reinterpret_cast<const void*>(decode_fast_kernel<BITS, WN, NS, MINB, GRP, 1, 1>),
                      NS, GRP, comb};
@@ -1341,7 +1372,7 @@ static Variant fast_kernel(const Geom& G, int ng, bool swp = true) {
                  : cp_knob == 2 ? ((ng <= 4 && (G.bits == 2 || G.bits == 4)) ? 2 : 1)
                                 : col_pack(G, ng);
 #define BDK_SEL(B, W, NS, MB, GR) \
-  if (G.bits == B && G.warp_n == W) return variant<B, W, NS, MB, GR>(cp, swp);
+  if (G.bits == B && G.warp_n == W) return variant<B, W, NS, MB, GR>(cp, swp, ng);
   if (v == 2) {
     BDK_SEL(2, 4, 8, 1, 2) BDK_SEL(4, 4, 8, 1, 2)
   } else if (v == 3) {
