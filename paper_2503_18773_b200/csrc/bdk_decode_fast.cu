@@ -389,7 +389,9 @@ __device__ __forceinline__ float fhfma(uint16_t a, uint16_t b, float c) {
 // lane's query channels as half2).  The params are (scale | zero << 16) u32
 // per channel; the zero terms take the high halves directly (FHFMA half
 // selects: no conversions, no repacking).
-template <int NH>
+// GPB: K groups per block, N_r / 128 -- a compile-time constant of the
+// kernel (N_r = 8 W_n (16 / bits), and the fast path has g = 128)
+template <int NH, int GPB>
 __device__ __forceinline__ void prep_fold(const uint8_t* rec, uint8_t* pp, const Geom& G, int ng,
                                           const uint32_t (&q2)[D / (32 / NH) / 2]) {
   constexpr int LPH = 32 / NH;  // lanes per head
@@ -397,8 +399,9 @@ __device__ __forceinline__ void prep_fold(const uint8_t* rec, uint8_t* pp, const
   constexpr int H2 = CPL / 2;   // half2 per lane
   const int lane = threadIdx.x & 31;
   const int h = lane % NH, cbk = lane / NH;
-  const int gpb = G.k_axis == 0 ? G.n_r / G.g : 1;
+  constexpr int gpb = GPB;
   const uint32_t* kp = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes);
+#pragma unroll
   for (int gr = 0; gr < gpb; ++gr) {
     uint8_t* qp = pp + gr * QP_BYTES;
     float za = 0.f, zb = 0.f;
@@ -466,7 +469,7 @@ struct PrepCtx {
 // NH = n_group rounded up to a power of two: lane -> (head lane % NH, a block
 // of 4*NH channels), so only real heads cost work; Q' rows of heads >= n_group
 // stay zero (prep areas are zeroed at kernel start).
-template <int NH, int NS, int GRP>
+template <int NH, int NS, int GRP, int GPB>
 __device__ __forceinline__ void prep_loop(const DevCache& c, const FastArgs& a, const PrepCtx& px) {
   constexpr int LPH = 32 / NH;  // lanes per head
   constexpr int CPL = D / LPH;  // channels per lane
@@ -502,7 +505,8 @@ __device__ __forceinline__ void prep_loop(const DevCache& c, const FastArgs& a, 
         const unsigned long long tb = (px.tr && lane == 0) ? globaltimer() : 0ull;
         if (px.tr && lane == 0) px.tr[12] += tb - tw;
         if (!(a.dev_flags & 2)) {
-          prep_fold<NH>(px.ring + (size_t)s * px.rec, px.prep + (size_t)s * px.prep_stride, G, ng, q2);
+          prep_fold<NH, GPB>(px.ring + (size_t)s * px.rec, px.prep + (size_t)s * px.prep_stride, G,
+                             ng, q2);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&px.ready[s]);
@@ -944,14 +948,16 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
     const int nh = ng <= 1 ? 1 : ng <= 2 ? 2 : ng <= 4 ? 4 : 8;
     PrepCtx px{ring, prep, full, ready, tr, REC, (int)L.prep_stride, pgrp, u_begin, u_end,
                so.off0, cell0, 16 * NC};
+    // K groups per block: N_r / 128 (fast_decode_ok: g = 128, N_r % g = 0)
+    constexpr int GPB = (WN * (16 / BITS)) / 16 > 0 ? (WN * (16 / BITS)) / 16 : 1;
     if constexpr (NHT > 0) {
       (void)nh;
-      prep_loop<NHT, NS, GRP>(c, a, px);
+      prep_loop<NHT, NS, GRP, GPB>(c, a, px);
     } else {
-      if (nh == 1) prep_loop<1, NS, GRP>(c, a, px);
-      else if (nh == 2) prep_loop<2, NS, GRP>(c, a, px);
-      else if (nh == 4) prep_loop<4, NS, GRP>(c, a, px);
-      else prep_loop<8, NS, GRP>(c, a, px);
+      if (nh == 1) prep_loop<1, NS, GRP, GPB>(c, a, px);
+      else if (nh == 2) prep_loop<2, NS, GRP, GPB>(c, a, px);
+      else if (nh == 4) prep_loop<4, NS, GRP, GPB>(c, a, px);
+      else prep_loop<8, NS, GRP, GPB>(c, a, px);
     }
     return;
   }
