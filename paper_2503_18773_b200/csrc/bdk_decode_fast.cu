@@ -66,6 +66,21 @@ struct FC {
   static constexpr int NC = WN * GRP_;         // consumer warps (+ TMA warp + GRP_ prep warps)
 };
 
+// Record geometry of the fast path, fixed by (bits, W_n): d = 128, g = 128,
+// KChannel K (fast_decode_ok), N_r = 8 W_n (16 / bits).  Word bytes per
+// tensor 16 W_n d, K params (N_r / 128) d (scale, zero) u16 pairs, V params
+// N_r pairs, the record padded to 128 B (bdk_api.cu's Geom, checked at launch)
+template <int BITS, int WN>
+struct FG {
+  static constexpr int NR = 8 * WN * (16 / BITS);
+  static constexpr int GPB = NR / 128 > 0 ? NR / 128 : 1;
+  static constexpr int WB = 16 * WN * 128;
+  static constexpr int KPB = GPB * 128 * 4;
+  static constexpr int VPB = NR * 4;
+  static constexpr int REC = (2 * WB + KPB + VPB + 127) / 128 * 128;
+  static constexpr int PREP_STRIDE = (GPB * (8 * 272 + 8 * 4) + 127) / 128 * 128;
+};
+
 struct Smem {
   uint32_t ring, prep, merge;  // byte offsets
   uint32_t prep_stride;
@@ -641,7 +656,8 @@ __device__ __forceinline__ void soft_stage(const uint8_t* rec, const Geom& G, in
   using T = Stg<BITS, WN, CP>;
   constexpr int P = T::P, NPK = T::NPK, SH_REF = T::SH_REF;
   const int lane = threadIdx.x & 31, gid = lane >> 2;
-  const uint32_t* vpr = reinterpret_cast<const uint32_t*>(rec + 2 * G.wbytes + G.kp_bytes);
+  using F = FG<BITS, WN>;
+  const uint32_t* vpr = reinterpret_cast<const uint32_t*>(rec + 2 * F::WB + F::KPB);
   softmax_update<NPK>(sacc, st, o);
   // ---- P' = P * s_t (V token scale folded), zero term, P'^T fragments
 #pragma unroll
@@ -682,7 +698,7 @@ __device__ __forceinline__ void ldv_stage(const uint8_t* rec, const Geom& G, int
                                           uint32_t (&vr)[4][4], uint64_t* empty_s) {
   constexpr int RB = Stg<BITS, WN, CP>::RB;
   const int lane = threadIdx.x & 31;
-  const uint32_t vw = smem_u32(rec + G.wbytes);
+  const uint32_t vw = smem_u32(rec + FG<BITS, WN>::WB);
 #pragma unroll
   for (int vc = 0; vc < 4; ++vc) {
     const int row = vc * 32 + lane;
@@ -854,7 +870,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
   long long* sched_sm =
       reinterpret_cast<long long*>(smem + L.total - 3 * NS * 8 - 48 - 128);  // [16]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t4 = lane & 3;
-  const int REC = G.rec_bytes;
+  constexpr int REC = FG<BITS, WN>::REC;  // == G.rec_bytes (checked at launch)
 
   // zero the prep areas once: Q' rows of heads >= n_group stay zero
   for (uint32_t i = threadIdx.x * 16; i < NS * L.prep_stride; i += blockDim.x * 16)
@@ -1024,7 +1040,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
           mbar_wait(&full[s], (it / NS) & 1);
           if (tr && threadIdx.x == 0 && it == 0) tr[1] = globaltimer();
           const uint8_t* rec = ring + (size_t)s * REC;
-          qk_stage<BITS, WN, CP>(rec, prep + (size_t)s * L.prep_stride + kgr * QP_BYTES, j, scale,
+          qk_stage<BITS, WN, CP>(rec, prep + (size_t)s * FG<BITS, WN>::PREP_STRIDE + kgr * QP_BYTES, j, scale,
                                  sacc);
           soft_stage<BITS, WN, CP>(rec, G, j, vtok, sacc, st, o, pb, pbh);
           ldv_stage<BITS, WN, CP>(rec, G, j, vr, &empty[s]);
@@ -1037,7 +1053,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
           mbar_wait(&full[s], (k / NS) & 1);
           if (tr && threadIdx.x == 0) tr[9] += globaltimer() - tw;
           const uint8_t* rec = ring + (size_t)s * REC;
-          qk_stage<BITS, WN, CP>(rec, prep + (size_t)s * L.prep_stride + kgr * QP_BYTES, j, scale,
+          qk_stage<BITS, WN, CP>(rec, prep + (size_t)s * FG<BITS, WN>::PREP_STRIDE + kgr * QP_BYTES, j, scale,
                                  sacc);
           pv_stage<BITS, WN, CP>(vr, pb, pbh, o);
           soft_stage<BITS, WN, CP>(rec, G, j, vtok, sacc, st, o, pb, pbh);
@@ -1064,7 +1080,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
         continue;
       }
       consume_block<BITS, WN, CP>(ring + (size_t)s * REC,
-                                  prep + (size_t)s * L.prep_stride + kgr * QP_BYTES, G, j, scale,
+                                  prep + (size_t)s * FG<BITS, WN>::PREP_STRIDE + kgr * QP_BYTES, G, j, scale,
                                   vtok, st, o, &empty[s]);
     }
 
@@ -1423,6 +1439,17 @@ cudaError_t launch_decode_fast(const DevCache& c, const FastArgs& a, cudaStream_
   const bool swp = a.dev_sched || a.total_units >= 2LL * a.n_ctas || swp_knob() == 2;
   const Variant k = fast_kernel(c.G, a.n_group, swp);
   if (!k.fn) return cudaErrorInvalidValue;
+  // the kernels bake the record geometry in (FG); it must be the cache's
+  {
+    const Geom& G = c.G;
+    const int P = 16 / G.bits, nr = 8 * G.warp_n * P, gpb = nr / 128 > 0 ? nr / 128 : 1;
+    const int rec = (2 * 16 * G.warp_n * 128 + gpb * 512 + nr * 4 + 127) / 128 * 128;
+    if (G.rec_bytes != rec || G.wbytes != 16 * G.warp_n * 128 || G.kp_bytes != gpb * 512 ||
+        G.n_r != nr || G.g != 128 || G.k_axis != 0 ||
+        (int)smem_layout(G, a.n_group, k.ns, k.grp).prep_stride !=
+            (gpb * QP_BYTES + 127) / 128 * 128)
+      return cudaErrorInvalidValue;
+  }
   const uint32_t smem = fast_smem(c.G, a.n_group, k);
   DevCache cc = c;
   FastArgs aa = a;
