@@ -1149,7 +1149,7 @@ __global__ void __maxnreg__(GRP >= 3 ? 128 : (MINB >= 3 ? 112 : 168))
 // finished a cell last.  CTA (cell, 0) then commits the cell's next lengths
 // into the other half of len2 and, when the step filled the residual window,
 // quantizes + packs it into the cell's next block slot (the fused flush).
-constexpr int CMB_LB = 48;  // contributors per load batch (one round for C1-C5)
+constexpr int CMB_LB = 40;  // contributors per load batch (one round for C1-C5: <= 38)
 
 template <int BITS, int WN>
 __global__ void __launch_bounds__(D) combine_fast_kernel(const __grid_constant__ DevCache c,
